@@ -1,0 +1,78 @@
+// swe_types.h — structures shared by the host runtime (swe_capi.cu) and the
+// step kernels.  Not part of the public C-ABI (include/swe_cuda.h).
+#pragma once
+
+#include <cstdint>
+
+#include "../../include/swe_cuda.h"
+
+enum { SWE_EDGE_N = 0, SWE_EDGE_S = 1, SWE_EDGE_E = 2, SWE_EDGE_W = 3 };
+
+struct SweBC {
+    int type;  // swe_bc_type
+    double q_n;
+    double eta_out;
+};
+
+// Reduction words, all combined with unsigned max (atomicMax on the device,
+// ncclMax across ranks).  Error indices are stored complemented (~idx) so that
+// max selects the row-major FIRST offender; 0 means "none".
+enum {
+    RED_SX = 0,   // bits of max sx = |qx/h| + sqrt(g h)   (non-negative doubles order like u64)
+    RED_SY = 1,   // bits of max sy
+    RED_E4 = 2,   // ~ first corrector cell consuming a dry U*   (executor.hpp:429-436)
+    RED_E5 = 3,   // ~ first guard offender                       (executor.hpp:543-556)
+    RED_E2 = 4,   // committed depth below h_min seen by the predictor (scheme.hpp:35-39)
+    RED_DIAG = 5, // K6 needs the exact per-cell scan (dx/sx underflow/overflow possible)
+    RED_N = 8
+};
+
+// Device control block: the committed-state bookkeeping of swe::Stepper
+// (executor.hpp:1106-1115) plus the run_from loop scalars (run.hpp:149-163),
+// kept on the device so a CUDA graph of step launches needs no host sync.
+struct __align__(16) SweCtl {
+    double t;                     // committed time
+    double dt_raw;                // raw CFL dt for the next step
+    double t_end;                 // advance(): landing target
+    double dt_req;                // step(): dt from the host
+    double tcommit_req;           // step(): committed time from the host
+    double dt_used, t_commit, dt_next;  // results of the last launch
+    double err_dt;                // StepCollapseError::dt
+    double err_t;                 // InstabilityError/StepCollapseError sim time
+    double max_sx, max_sy;        // CFL maxima of the last launch (diagnosis)
+    unsigned long long step_index;  // parity of the next step
+    unsigned long long steps_done;  // committed steps since the counter was reset
+    int sel;                      // committed buffer (0/1)
+    int done;                     // 1 => further launches are no-ops
+    int mode;                     // 0 host step, 1 advance
+    int status;                   // swe_code of the last launch, 7 = needs host diagnosis
+    int err_kind;                 // 2/4/5/6: which plan kernel raised
+    int err_i, err_j;
+    unsigned int finish;          // CTA arrival counter for the last-block finalize
+    unsigned long long red[RED_N];
+};
+
+#define SWE_STATUS_DIAG 7
+
+// Kernel parameters (passed by value as a __grid_constant__).
+struct StepParams {
+    double* buf[2];        // committed/candidate state, row-interleaved SoA
+    const double* slope;   // dzdx/dzdy rows, same layout; nullptr for a flat bed
+    const double* z_w;     // bed z at i=0 per local row
+    const double* z_e;     // bed z at i=nx-1 per local row
+    const double* z_s;     // bed z at global row 0 per column
+    const double* z_n;     // bed z at global row ny-1 per column
+    SweCtl* ctl;
+    int nx, ny;            // global grid
+    int nloc, j0;          // rows owned by this rank: global [j0, j0+nloc)
+    int pitch;             // doubles per field row (P)
+    int ntiles;            // x tiles
+    int ncta;              // CTAs launched
+    int finalize;          // 1: last CTA finalizes (one rank); 0: host-side allreduce + finalize kernel
+    int nranks;
+    double dx, dy, g, half_g, neg_g, gnn, h_min, nu;
+    double cfl, dt_max, dt_min;
+    double tz_x, tz_y;     // K6 diagnosis triggers (dx/sx would round to 0)
+    int always_diag;       // pathological parameters: diagnose every step
+    SweBC bc[4];           // N, S, E, W
+};
