@@ -47,6 +47,9 @@ __device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned
                  "r"(bytes)
                  : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
     asm volatile(
         "{\n\t.reg .pred P1;\n"
@@ -151,8 +154,10 @@ __device__ __forceinline__ void finalize_step(const StepParams& p, SweCtl* c, do
 }
 
 // --------------------------------------------------------------- the kernel
+// Block = NT compute threads (one column each) + one producer warp that
+// streams committed rows into the shared-memory ring with TMA bulk copies.
 template <int NT, bool FWD, bool SMOOTH, bool FLAT, bool MANNING>
-__global__ void __launch_bounds__(NT) swe_step_kernel(const __grid_constant__ StepParams p) {
+__global__ void __launch_bounds__(NT + 32, 3) swe_step_kernel(const __grid_constant__ StepParams p) {
     constexpr int R = SMOOTH ? 2 : 1;
     constexpr int S = FWD ? 1 : -1;
     constexpr int NF = FLAT ? 3 : 5;
@@ -164,8 +169,9 @@ __global__ void __launch_bounds__(NT) swe_step_kernel(const __grid_constant__ St
     double* xF = stage + D * NF * NT;                     // [2][3][NT] committed F (qx, fxx, fxy)
     double* xH = xF + 2 * 3 * NT;                         // [2][3][NT] x-interface fluxes
     double* xC = xH + 2 * 3 * NT;                         // [2][3][NT] corrector output (SMOOTH)
-    unsigned long long* bars =
+    unsigned long long* bars =  // [D] full, [D] empty
         reinterpret_cast<unsigned long long*>(xC + (SMOOTH ? 2 * 3 * NT : 0));
+    unsigned long long* ebars = bars + D;
 
     __shared__ Seg segs[MAXSEG];
     __shared__ int s_nseg, s_skip, s_sel, s_last;
@@ -197,7 +203,10 @@ __global__ void __launch_bounds__(NT) swe_step_kernel(const __grid_constant__ St
         s_tc = tc;
         s_sel = vc->sel;
         s_nseg = seg_list(p, blockIdx.x, segs, MAXSEG);
-        for (int d = 0; d < D; ++d) mbar_init(&bars[d], 1);
+        for (int d = 0; d < D; ++d) {
+            mbar_init(&bars[d], 1);
+            mbar_init(&ebars[d], NT / 32);
+        }
         fence_mbar_init();
     }
     __syncthreads();
@@ -211,42 +220,40 @@ __global__ void __launch_bounds__(NT) swe_step_kernel(const __grid_constant__ St
     const int nseg = s_nseg;
     const double h_min = p.h_min, half_g = p.half_g, neg_g = p.neg_g, gnn = p.gnn;
 
-    // ---- producer: request n -> (segment, row); L + 2R requests per segment
-    auto req_loc = [&](int n, int& tile, int& row) -> bool {
-        for (int k = 0; k < nseg; ++k) {
-            const int cnt = (segs[k].rb - segs[k].ra) + 2 * R;
-            if (n < cnt) {
-                tile = segs[k].tile;
-                row = FWD ? segs[k].ra - R + n : segs[k].rb - 1 + R - n;
-                return true;
-            }
-            n -= cnt;
-        }
-        return false;
-    };
-    auto issue = [&](int n) {
-        int tile, row;
-        if (!req_loc(n, tile, row)) return;
-        const int d = n % D;
-        double* dst = stage + d * NF * NT;
-        const size_t col0 = static_cast<size_t>(tile) * (NT - 2 * R);  // padded offset of x0-R
-        const size_t rbase = static_cast<size_t>(row + R) * 3;
-        mbar_expect_tx(&bars[d], NF * NT * 8);
-        for (int f = 0; f < 3; ++f)
-            bulk_g2s(dst + f * NT, cur + (rbase + f) * P + col0, NT * 8, &bars[d]);
-        if constexpr (!FLAT) {
-            const size_t sbase = static_cast<size_t>(row + R) * 2;
-            for (int f = 0; f < 2; ++f)
-                bulk_g2s(dst + (3 + f) * NT, p.slope + (sbase + f) * P + col0, NT * 8, &bars[d]);
-        }
-    };
-    if (tid == 0)
-        for (int n = 0; n < D; ++n) issue(n);
-
     int req = 0;  // next request to consume
     double mx = 0.0, my = 0.0;
     unsigned long long e2 = 0, e4 = 0, e5 = 0;
 
+    if (tid >= NT) {
+        // ---- producer warp: request n = (segment, row), L + 2R per segment, in
+        // consumption order; stage n % D is refilled once every compute warp
+        // has released request n - D (empty barrier).
+        if (tid == NT) {
+            int n = 0;
+            for (int k = 0; k < nseg; ++k) {
+                const int cnt = (segs[k].rb - segs[k].ra) + 2 * R;
+                const size_t col0 = static_cast<size_t>(segs[k].tile) * (NT - 2 * R);  // padded x0-R
+                for (int m = 0; m < cnt; ++m, ++n) {
+                    const int row = FWD ? segs[k].ra - R + m : segs[k].rb - 1 + R - m;
+                    const int d = n % D;
+                    if (n >= D) mbar_wait(&ebars[d], static_cast<unsigned>(((n / D) - 1) & 1));
+                    double* dst = stage + d * NF * NT;
+                    const double* src = cur + static_cast<size_t>(row + R) * 3 * P + col0;
+                    mbar_expect_tx(&bars[d], NF * NT * 8);
+                    bulk_g2s(dst, src, NT * 8, &bars[d]);
+                    bulk_g2s(dst + NT, src + P, NT * 8, &bars[d]);
+                    bulk_g2s(dst + 2 * NT, src + 2 * P, NT * 8, &bars[d]);
+                    if constexpr (!FLAT) {
+                        const double* ss = p.slope + static_cast<size_t>(row + R) * 2 * P + col0;
+                        bulk_g2s(dst + 3 * NT, ss, NT * 8, &bars[d]);
+                        bulk_g2s(dst + 4 * NT, ss + P, NT * 8, &bars[d]);
+                    }
+                }
+            }
+        }
+    } else {
+
+    const unsigned lane = tid & 31u;
     auto consume = [&](CellVec& u, double& zx, double& zy) {
         const int d = req % D;
         mbar_wait(&bars[d], static_cast<unsigned>((req / D) & 1));
@@ -261,10 +268,10 @@ __global__ void __launch_bounds__(NT) swe_step_kernel(const __grid_constant__ St
             zx = 0.0;
             zy = 0.0;
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ebars[d]);
     };
-    auto refill = [&]() {  // after a __syncthreads: the stage of request req-1 is free
-        if (tid == 0 && req - 1 + D >= D) issue(req - 1 + D);
-    };
+    auto csync = [&]() { asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory"); };
 
     for (int sgi = 0; sgi < nseg; ++sgi) {
         const Seg sg = segs[sgi];
@@ -275,6 +282,9 @@ __global__ void __launch_bounds__(NT) swe_step_kernel(const __grid_constant__ St
         const bool corr_x = tid >= 1 && tid < NT - 1;
         const bool star_ok = FWD ? (tid < NT - 1) : (tid > 0);
         const int r_start = FWD ? sg.ra : sg.rb - 1;
+        // CTA-uniform: does this window touch the west/east domain edge?
+        const int xw0 = sg.tile * (NT - 2 * R) - R;
+        const bool xedge_cta = (xw0 <= 0) || (xw0 + NT - 1 >= p.nx - 1);
         constexpr int E = R;             // warm-up rows
         constexpr int X = SMOOTH ? 1 : 0;  // extra trailing iteration
         constexpr int KC = SMOOTH ? -1 : 0;
@@ -292,8 +302,7 @@ __global__ void __launch_bounds__(NT) swe_step_kernel(const __grid_constant__ St
         xF[(par * 3 + 0) * NT + tid] = U.qx;
         xF[(par * 3 + 1) * NT + tid] = FU.fxx;
         xF[(par * 3 + 2) * NT + tid] = FU.fxy;
-        __syncthreads();
-        refill();
+        csync();
 
         CellVec Hyp = {0.0, 0.0, 0.0};
         CellVec Cp = {0.0, 0.0, 0.0}, Cpp = {0.0, 0.0, 0.0};
@@ -359,8 +368,7 @@ __global__ void __launch_bounds__(NT) swe_step_kernel(const __grid_constant__ St
             xF[((par ^ 1) * 3 + 0) * NT + tid] = Un.qx;
             xF[((par ^ 1) * 3 + 1) * NT + tid] = FN.fxx;
             xF[((par ^ 1) * 3 + 2) * NT + tid] = FN.fxy;
-            __syncthreads();
-            refill();
+            csync();
 
             // 4. corrector  executor.hpp:451-519, scheme.hpp:185-191
             CellVec C = {0.0, 0.0, 0.0};
@@ -373,7 +381,8 @@ __global__ void __launch_bounds__(NT) swe_step_kernel(const __grid_constant__ St
                 Hxx.qy = xH[(par * 3 + 2) * NT + to];
                 CellVec hw = FWD ? Hxx : Hxo, he = FWD ? Hxo : Hxx;
                 CellVec hs = FWD ? Hyp : Hyn, hn = FWD ? Hyn : Hyp;
-                if (in_x && row_in) {
+                const bool yedge_row = (j == 0) || (j == p.ny - 1);
+                if ((xedge_cta || yedge_row) && in_x && row_in) {
                     const bool west = (i == 0), east = (i == p.nx - 1);
                     const bool south = (j == 0), north = (j == p.ny - 1);
                     if (west | east | south | north) {
@@ -460,8 +469,10 @@ __global__ void __launch_bounds__(NT) swe_step_kernel(const __grid_constant__ St
                 // K6 executor.hpp:560-580
                 const Recip rc = make_recip(o.h);
                 const double c = __dsqrt_rn(p.g * o.h);
-                const double sx = fabs(div_rn_z(o.qx, rc)) + c;
-                const double sy = fabs(div_rn_z(o.qy, rc)) + c;
+                double u, v;
+                div2(o.qx, o.qy, rc, u, v);
+                const double sx = fabs(u) + c;
+                const double sy = fabs(v) + c;
                 mx = fmax(mx, sx);
                 my = fmax(my, sy);
                 const size_t rb = static_cast<size_t>(rr + R) * 3;
@@ -470,6 +481,7 @@ __global__ void __launch_bounds__(NT) swe_step_kernel(const __grid_constant__ St
                 nxt[(rb + 1) * P + col] = o.qx;
                 nxt[(rb + 2) * P + col] = o.qy;
                 // K1 of the next step: ghosts of the committed candidate
+                if (!(xedge_cta || jj == 0 || jj == p.ny - 1)) return;
                 if (i == 0) {
                     const CellVec g = edge_ghost(SWE_EDGE_W, p.bc[SWE_EDGE_W], o, p.z_w[rr + R], h_min);
                     nxt[(rb + 0) * P + col - 1] = g.h;
@@ -513,10 +525,12 @@ __global__ void __launch_bounds__(NT) swe_step_kernel(const __grid_constant__ St
                           xC[(pp * 3 + 2) * NT + tid - 1]};
                     Cn = FWD ? C : Cpp;
                     Cs = FWD ? Cpp : C;
+                    if (xedge_cta || jq == 0 || jq == p.ny - 1) {
                     if (i == 0) Cw = edge_ghost(SWE_EDGE_W, p.bc[SWE_EDGE_W], Cp, p.z_w[q + R], h_min);
                     if (i == p.nx - 1) Ce = edge_ghost(SWE_EDGE_E, p.bc[SWE_EDGE_E], Cp, p.z_e[q + R], h_min);
                     if (jq == 0) Cs = edge_ghost(SWE_EDGE_S, p.bc[SWE_EDGE_S], Cp, p.z_s[i], h_min);
                     if (jq == p.ny - 1) Cn = edge_ghost(SWE_EDGE_N, p.bc[SWE_EDGE_N], Cp, p.z_n[i], h_min);
+                    }
                     const double nu = p.nu;
                     CellVec o;
                     o.h = Cp.h + nu * (((Ce.h - Cp.h) + (Cw.h - Cp.h)) + ((Cn.h - Cp.h) + (Cs.h - Cp.h)));
@@ -541,15 +555,16 @@ __global__ void __launch_bounds__(NT) swe_step_kernel(const __grid_constant__ St
             Hyp = Hyn;
             par ^= 1;
         }
-        __syncthreads();  // smem exchange slots are reused by the next segment
+        csync();  // smem exchange slots are reused by the next segment
     }
+    }  // compute threads
 
     // ---- CTA reduction of the CFL maxima and error words
     for (int o = 16; o > 0; o >>= 1) {
         mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         my = fmax(my, __shfl_xor_sync(0xffffffffu, my, o));
     }
-    if ((tid & 31) == 0) {
+    if ((tid & 31) == 0 && tid < NT) {
         s_red[0][tid >> 5] = mx;
         s_red[1][tid >> 5] = my;
     }
@@ -583,7 +598,7 @@ __global__ void __launch_bounds__(NT) swe_step_kernel(const __grid_constant__ St
 template <int NT, bool FWD, bool SMOOTH, bool FLAT>
 constexpr size_t step_smem_bytes() {
     return static_cast<size_t>(kStages) * (FLAT ? 3 : 5) * NT * 8 + 2 * 3 * NT * 8 * (SMOOTH ? 3 : 2) +
-           kStages * 8;
+           2 * kStages * 8;
 }
 
 }  // namespace swe_dev

@@ -22,7 +22,7 @@ cudaError_t launch_one(int grid, cudaStream_t s, const StepParams& p) {
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    k<<<grid, kNT, smem, s>>>(p);
+    k<<<grid, kNT + 32, smem, s>>>(p);
     return cudaGetLastError();
 }
 
@@ -32,7 +32,7 @@ int occupancy_one() {
     auto k = swe_dev::swe_step_kernel<kNT, FWD, SMOOTH, FLAT, MANNING>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kNT, smem) != cudaSuccess) return 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kNT + 32, smem) != cudaSuccess) return 1;
     return n > 0 ? n : 1;
 }
 

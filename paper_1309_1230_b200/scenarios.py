@@ -41,12 +41,20 @@ def dam_break(spec: GridSpec, split_x: float, h_left: float, h_right: float) -> 
 
 
 class Scenario:
+    """ScenarioConfig subset (scenarios.hpp:57-70).  `ic(spec)` builds the initial
+    state on a grid; every IC here is uniform along y, so build_rows() can
+    materialise one rank's strip without the full grid."""
+
     def __init__(self, name, spec, phys, pol, bounds, t_end, ic):
         self.name, self.spec, self.phys, self.pol, self.bounds, self.t_end, self.ic = (
             name, spec, phys, pol, bounds, t_end, ic)
 
     def build(self) -> FieldSet:
-        return self.ic()
+        return self.ic(self.spec)
+
+    def build_rows(self, r0: int, r1: int) -> FieldSet:
+        s = self.spec
+        return self.ic(GridSpec(s.nx, r1 - r0, s.dx, s.dy))
 
 
 def gen_channel_flood(n: int = 1024, manning_n: float = 0.035) -> Scenario:
@@ -56,7 +64,7 @@ def gen_channel_flood(n: int = 1024, manning_n: float = 0.035) -> Scenario:
     bounds = BoundarySet(north=BoundaryKind.wall(), south=BoundaryKind.wall(),
                          east=BoundaryKind.fixed_eta(1.0), west=BoundaryKind.inflow(0.1, 1.0))
     return Scenario("channel-flood", spec, PhysicsParams(manning_n=manning_n), StabilityPolicy(cfl=SCENARIO_CFL),
-                    bounds, 1000.0, lambda: channel_slope(spec, 1.0, slope))
+                    bounds, 1000.0, lambda sp: channel_slope(sp, 1.0, slope))
 
 
 def gen_square_dam(n: int, h_left: float = 1.0, h_right: float = 0.5, nu_art: float = 0.0,
@@ -65,7 +73,7 @@ def gen_square_dam(n: int, h_left: float = 1.0, h_right: float = 0.5, nu_art: fl
     spec = GridSpec(n, n, 1.0, 1.0)
     sx = 0.5 * n * spec.dx if split_x is None else split_x
     return Scenario("square-dam", spec, PhysicsParams(nu_art=nu_art), StabilityPolicy(cfl=SCENARIO_CFL),
-                    BoundarySet.all(BoundaryKind.wall()), 1e18, lambda: dam_break(spec, sx, h_left, h_right))
+                    BoundarySet.all(BoundaryKind.wall()), 1e18, lambda sp: dam_break(sp, sx, h_left, h_right))
 
 
 def gen_dam_break(n: int = 400, h_l: float = 1.0, h_r: float = 0.5) -> Scenario:
@@ -77,7 +85,7 @@ def gen_dam_break(n: int = 400, h_l: float = 1.0, h_r: float = 0.5) -> Scenario:
     split = 0.5 * n * spec.dx
     t_end = 0.25 * n * spec.dx / math.sqrt(phys.g * h_l)
     return Scenario("dam-break", spec, phys, StabilityPolicy(cfl=SCENARIO_CFL), bounds, t_end,
-                    lambda: dam_break(spec, split, h_l, h_r))
+                    lambda sp: dam_break(sp, split, h_l, h_r))
 
 
 def gen_floodplain(n: int = 16384) -> Scenario:
