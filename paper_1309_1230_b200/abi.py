@@ -8,7 +8,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libswe_cuda.so")
+LIB_PATH = os.environ.get("SWE_CUDA_LIB") or os.path.join(HERE, "lib", "libswe_cuda.so")
 
 SWE_OK = 0
 SWE_ERR_CONFIG = 2

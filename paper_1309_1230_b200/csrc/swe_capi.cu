@@ -262,7 +262,7 @@ struct swe_ctx {
     swe_boundary_set bnd{};
     swe_exec ex{};
     int R = 1, nloc = 0, j0 = 0, pitch = 0, ntiles = 0;
-    bool smooth = false, manning = false, flat = true, loaded = false;
+    bool smooth = false, manning = false, flat = true, loaded = false, exact = true;
     int clamp_any = 0;
     int warnings_total = 0;
     double t = 0.0;
@@ -403,7 +403,7 @@ int halo_exchange(swe_ctx* c, int which, swe_status* st) {
 // exchange only).
 int enqueue_step(swe_ctx* c, bool fwd, int cand, swe_status* st) {
     const int v = swe_step_variant(fwd, c->smooth, c->flat, c->manning);
-    CUDA_TRY(swe_launch_step(v, c->ncta, c->stream, c->prm));
+    CUDA_TRY(swe_launch_step(c->exact, v, c->ncta, c->stream, c->prm));
     ++c->launches;
     if (c->ex.nranks > 1) {
         NCCL_TRY(g_nccl.AllReduce(c->d_ctl->red, c->d_ctl->red, RED_N, ncclUint64, ncclMax, c->comm,
@@ -609,14 +609,15 @@ EXPORT int swe_cuda_create(const swe_grid* grid, const swe_physics* phys, const 
     c->bnd = *bnd;
     c->ex = ex;
     c->ex.nccl_id = nullptr;
+    c->exact = (ex.flags & SWE_EXEC_EXACT) != 0;
     c->smooth = phys->nu_art > 0.0;  // StepPlan::standard(nu_art > 0), executor.hpp:730
     c->manning = phys->manning_n > 0.0;
     c->R = c->smooth ? 2 : 1;
     c->j0 = bands[ex.rank].first;
     c->nloc = bands[ex.rank].second - bands[ex.rank].first;
-    const int out_w = SWE_STEP_NT - 2 * c->R;
+    const int out_w = SWE_TILE_W(c->R);
     c->ntiles = (grid->nx + out_w - 1) / out_w;
-    c->pitch = ((c->ntiles * out_w + 2 * c->R + SWE_STEP_NT) + 31) / 32 * 32;
+    c->pitch = ((c->ntiles * out_w + 2 * c->R + 32) + 31) / 32 * 32;
     const size_t rows = static_cast<size_t>(c->nloc + 2 * c->R);
     c->buf_doubles = rows * 3 * c->pitch;
     *out = c;
@@ -833,16 +834,27 @@ EXPORT int swe_cuda_load(swe_ctx* c, const double* z, const double* h, const dou
 
     // occupancy-sized persistent grid
     const int v = swe_step_variant(true, c->smooth, c->flat, c->manning);
-    c->occ = swe_step_occupancy(v);
+    c->occ = swe_step_occupancy(c->exact, v);
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->ex.device);
+    // persistent grid: every resident warp is a worker; small grids keep at
+    // least 4 rows per worker so the 2R warm-up rows stay amortised
     const long long units = static_cast<long long>(c->ntiles) * nloc;
-    const long long want = std::max<long long>(1, units / 4);
+    const long long want = std::max<long long>(1, units / (4 * SWE_STEP_WPB));
     long long ncta = std::min<long long>(static_cast<long long>(c->occ) * nsm, want);
-    // every CTA must span at most 7 tiles (MAXSEG = 8 segments)
-    ncta = std::max<long long>(ncta, (c->ntiles + 6) / 7);
+    // every worker must span at most 7 tiles (MAXSEG = 8 segments)
+    ncta = std::max<long long>(ncta, (c->ntiles + 7 * SWE_STEP_WPB - 1) / (7 * SWE_STEP_WPB));
     c->ncta = static_cast<int>(ncta);
     c->prm.ncta = c->ncta;
+    // dynamic work items: ~16 per worker, 16..128 rows each
+    {
+        const long long workers = ncta * SWE_STEP_WPB;
+        long long ch = units / std::max<long long>(1, workers * 16);
+        ch = std::max<long long>(16, std::min<long long>(128, ch));
+        ch = std::min<long long>(ch, nloc);
+        c->prm.chunk = static_cast<int>(ch);
+        c->prm.nchunks = static_cast<int>((nloc + ch - 1) / ch);
+    }
     destroy_graphs(c);  // variant may have changed
 
     std::memset(c->h_ctl, 0, sizeof(SweCtl));

@@ -1,16 +1,28 @@
 // swe_launch.h — internal launcher interface between the host runtime and the
-// step-kernel instantiations.
+// step-kernel instantiations (swe_step_inst.cu, compiled once per mode).
 #pragma once
 
 #include <cuda_runtime.h>
 
 #include "swe_types.h"
 
-#ifndef SWE_STEP_NT
-#define SWE_STEP_NT 128
+#ifndef SWE_STEP_WPB
+#define SWE_STEP_WPB 4   // warps per CTA; every warp is an independent row-march worker
 #endif
+#define SWE_TILE_W(R) (32 - 2 * (R))  // output columns per warp window
 
-int swe_step_variant(bool fwd, bool smooth, bool flat, bool manning);
-cudaError_t swe_launch_step(int variant, int grid, cudaStream_t stream, const StepParams& p);
-int swe_step_occupancy(int variant);
+inline int swe_step_variant(bool fwd, bool smooth, bool flat, bool manning) {
+    return (fwd ? 8 : 0) | (smooth ? 4 : 0) | (flat ? 2 : 0) | (manning ? 1 : 0);
+}
+cudaError_t swe_launch_step_exact(int variant, int grid, cudaStream_t stream, const StepParams& p);
+cudaError_t swe_launch_step_fast(int variant, int grid, cudaStream_t stream, const StepParams& p);
+int swe_step_occupancy_exact(int variant);
+int swe_step_occupancy_fast(int variant);
 cudaError_t swe_launch_finalize(cudaStream_t stream, const StepParams& p);
+
+inline cudaError_t swe_launch_step(bool exact, int variant, int grid, cudaStream_t stream, const StepParams& p) {
+    return exact ? swe_launch_step_exact(variant, grid, stream, p) : swe_launch_step_fast(variant, grid, stream, p);
+}
+inline int swe_step_occupancy(bool exact, int variant) {
+    return exact ? swe_step_occupancy_exact(variant) : swe_step_occupancy_fast(variant);
+}

@@ -8,10 +8,12 @@
 //   K1   ghosts of the committed state are written by the previous step's
 //        epilogue (or the load kernel) into the padded buffer, so the
 //        predictor reads them as ordinary cells.
-//   K2+K4 fused per CTA with row marching: a CTA owns a 128-column window and
-//        walks a contiguous run of rows in the sweep direction.  Each state's
-//        fluxes F/G are evaluated once per cell and shared: x-neighbours
-//        through shared memory, y-neighbours in registers.  Interface fluxes
+//   K2+K4 fused per warp with row marching: a warp owns a 32-column window
+//        (30 output columns, 28 with smoothing) and walks a contiguous run of
+//        rows in the sweep direction, independently of every other warp (no
+//        CTA barriers).  Each state's fluxes F/G are evaluated once per cell
+//        and shared: x-neighbours through warp shuffles, y-neighbours in
+//        registers.  Interface fluxes
 //        H_{i+1/2} are evaluated once per interface (the reference computes
 //        them twice, bit-identically: README.md:191-196).
 //   K3   U* ghosts are formed in-thread at domain edges only.
@@ -22,7 +24,7 @@
 //   Finalize: the last CTA to finish turns the reduction words into
 //        StepResult / errors and commits by flipping the ping-pong selector
 //        in the device control block (executor.hpp:836-840).
-// Committed rows arrive through a 4-stage cp.async.bulk (TMA bulk copy)
+// Committed rows arrive through a per-warp cp.async.bulk (TMA bulk copy)
 // ring with mbarrier completion; stores are coalesced 8-byte STG.
 #pragma once
 
@@ -30,7 +32,10 @@
 
 namespace swe_dev {
 
-constexpr int kStages = 4;
+constexpr int kStages = 5;
+#ifndef SWE_MINB
+#define SWE_MINB 3
+#endif
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -69,16 +74,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 }
 
 // ------------------------------------------------------------ work partition
-// CTA b owns units [b*U/G, (b+1)*U/G) of the unit space u = tile*nloc + row.
-// A unit run is split into segments at tile boundaries.
+// Worker w (one warp) owns units [w*U/G, (w+1)*U/G) of the unit space
+// u = tile*nloc + row.  A unit run is split into segments at tile boundaries.
 struct Seg {
     int tile, ra, rb;
 };
 
-__device__ __forceinline__ int seg_list(const StepParams& p, int b, Seg* segs, int maxseg) {
+__device__ __forceinline__ int seg_list(const StepParams& p, long long w, long long nw, Seg* segs,
+                                        int maxseg) {
     const long long total = static_cast<long long>(p.ntiles) * p.nloc;
-    long long u = total * b / p.ncta;
-    const long long u1 = total * (b + 1) / p.ncta;
+    long long u = total * w / nw;
+    const long long u1 = total * (w + 1) / nw;
     int n = 0;
     while (u < u1 && n < maxseg) {
         const int tile = static_cast<int>(u / p.nloc);
@@ -150,36 +156,492 @@ __device__ __forceinline__ void finalize_step(const StepParams& p, SweCtl* c, do
     }
     for (int k = 0; k < RED_N; ++k) red[k] = 0ull;
     c->finish = 0u;
+    c->work = 0u;
     __threadfence();
 }
 
 // --------------------------------------------------------------- the kernel
-// Block = NT compute threads (one column each) + one producer warp that
-// streams committed rows into the shared-memory ring with TMA bulk copies.
-template <int NT, bool FWD, bool SMOOTH, bool FLAT, bool MANNING>
-__global__ void __launch_bounds__(NT + 32, 3) swe_step_kernel(const __grid_constant__ StepParams p) {
-    constexpr int R = SMOOTH ? 2 : 1;
-    constexpr int S = FWD ? 1 : -1;
-    constexpr int NF = FLAT ? 3 : 5;
+// One warp = one worker.  Lane t owns column i = x0 - R + t of a 32-column
+// window; lanes R..31-R are output columns.  Iteration k of the row march is
+// a 3-stage software pipeline over consecutive rows (march direction S):
+//   stage 1  row b+S : committed row from the warp's TMA ring; F/G/S(U)
+//   stage 2  row b   : predictor U*, F/G/S(U*), interface fluxes, boundary
+//                      faces, dry-U* detection
+//   stage 3  row b-S : corrector (+ smoothing of row b-2S), guard, CFL, store
+// The three dependency chains interleave within the warp; x neighbours are
+// exchanged with shuffles, so warps never wait for each other.  The steady
+// state is unrolled by two with the pipeline registers ping-ponging between
+// two carry sets, so no register moves are needed to advance the march.
+
+// Pipeline registers entering an iteration.
+struct Carry {
+    CellVec U;                 // committed state of the stage-2 row b
+    Flux FU;                   // its fluxes
+    double srx, sry, zx, zy;   // its source term and bed slopes
+    CellVec Hyp;               // y face (b-S, b)
+    CellVec Uc;                // committed state of the stage-3 row c = b-S
+    double c_srx, c_sry, c_ssx, c_ssy;  // S(U) and S(U*) of row c
+    CellVec c_hs, c_hn, c_hx;  // y faces and own x face of row c
+    CellVec Cp, Cpp;           // corrector output of rows c-S, c-2S (smoothing)
+};
+
+struct WarpRing {  // per-warp TMA ring state (warp-uniform)
+    int d;         // stage of the next request to consume
+    unsigned ph;   // its mbarrier phase parity
+};
+
+template <int WPB, bool FWD, bool SMOOTH, bool FLAT, bool MANNING, bool EXACT>
+struct Marcher {
+    using A = Arith<EXACT>;
+    using Rc = typename A::Rc;
+    static constexpr int R = SMOOTH ? 2 : 1;
+    static constexpr int S = FWD ? 1 : -1;
+    static constexpr int NF = FLAT ? 3 : 5;
+    static constexpr int D = kStages;
+    static constexpr int TW = 32 - 2 * R;
+    static constexpr unsigned FULL = 0xffffffffu;
+
+    const StepParams& p;
+    double* stage;
+    unsigned long long* bars;
+    Seg* segq;      // per-warp queue of claimed work items (ring of QN)
+    int qhead, qtail;  // consumer / producer positions (warp-uniform)
+    int lane;
+    const double* cur;
+    double* nxt;
+    int P;
+    double dt, dtdx, dtdy, half_dt, h_min, half_g, neg_g, gnn;
+    // producer state (lanes < NF): next request
+    int pleft;
+    bool pdone;
+    const double* psrc;
+    long long pstep;
+    int pn, req;
+    WarpRing ring;
+    // per-segment constants
+    int i, L, r_start;
+    bool in_x, out_x, star_ok, xedge;
+    // reductions
+    double mx, my;
+    unsigned long long e2, e4, e5;
+
+    __device__ __forceinline__ double shf_nb(double x) const {
+        return FWD ? __shfl_down_sync(FULL, x, 1) : __shfl_up_sync(FULL, x, 1);
+    }
+    __device__ __forceinline__ double shf_back(double x) const {
+        return FWD ? __shfl_up_sync(FULL, x, 1) : __shfl_down_sync(FULL, x, 1);
+    }
+    static __device__ __forceinline__ double avg(double a, double b) { return 0.5 * (a + b); }
+
+    static constexpr int QN = 4;
+    // Producer: claim the next work item (tile, row chunk) from the step's
+    // atomic counter, queue it for the consumer and point this lane at its
+    // first row.  Dynamic claiming balances the cheaper interior windows
+    // against the boundary windows and any per-SM speed differences.
+    __device__ __forceinline__ void prod_seg() {
+        unsigned item = 0;
+        if (lane == 0) item = atomicAdd(&p.ctl->work, 1u);
+        item = __shfl_sync(FULL, item, 0);
+        const unsigned nitems = static_cast<unsigned>(p.ntiles) * static_cast<unsigned>(p.nchunks);
+        if (item >= nitems) {
+            pleft = 0;
+            pdone = true;
+            return;
+        }
+        const int rc = static_cast<int>(item / p.ntiles);   // row-chunk major: neighbouring
+        const int tile = static_cast<int>(item % p.ntiles); // windows share halo sectors in L2
+        Seg sg;
+        sg.tile = tile;
+        sg.ra = rc * p.chunk;
+        sg.rb = min(sg.ra + p.chunk, p.nloc);
+        segq[qtail % QN] = sg;
+        ++qtail;
+        pleft = (sg.rb - sg.ra) + 2 * R;
+        const int row = FWD ? sg.ra - R : sg.rb - 1 + R;
+        const size_t col0 = static_cast<size_t>(sg.tile) * TW;  // padded offset of x0-R
+        if (lane < 3) {
+            psrc = cur + (static_cast<size_t>(row + R) * 3 + lane) * P + col0;
+            pstep = static_cast<long long>(S) * 3 * P;
+        } else {
+            psrc = p.slope + (static_cast<size_t>(row + R) * 2 + (lane - 3)) * P + col0;
+            pstep = static_cast<long long>(S) * 2 * P;
+        }
+    }
+    __device__ __forceinline__ void produce() {
+        while (pn < req + D - 1) {
+            if (pleft == 0) {
+                if (pdone || qtail - qhead >= QN - 1) return;
+                prod_seg();
+                if (pleft == 0) return;
+            }
+            const int d = pn % D;
+            if (lane == 0) mbar_expect_tx(&bars[d], NF * 32 * 8);
+            __syncwarp();
+            if (lane < NF) bulk_g2s(stage + (d * NF + lane) * 32, psrc, 32 * 8, &bars[d]);
+            psrc += pstep;
+            --pleft;
+            ++pn;
+        }
+    }
+    __device__ __forceinline__ void consume(CellVec& u, double& zx, double& zy) {
+        mbar_wait(&bars[ring.d], ring.ph);
+        const double* st = stage + ring.d * NF * 32;
+        u.h = st[lane];
+        u.qx = st[32 + lane];
+        u.qy = st[64 + lane];
+        if constexpr (!FLAT) {
+            zx = st[96 + lane];
+            zy = st[128 + lane];
+        } else {
+            zx = 0.0;
+            zy = 0.0;
+        }
+        if (++ring.d == D) {
+            ring.d = 0;
+            ring.ph ^= 1u;
+        }
+        ++req;
+        __syncwarp();
+        produce();
+    }
+
+    // output cell: guard (K5), CFL (K6), store, ghosts for the next step (K1)
+    __device__ __forceinline__ void emit(const CellVec& o, int rr) {
+        const int jj = p.j0 + rr;
+        const bool ok = finite_d(o.h) && finite_d(o.qx) && finite_d(o.qy) && o.h >= h_min;
+        if (!ok) e5 = max(e5, ~(static_cast<unsigned long long>(jj) * p.nx + i));
+        const Rc rc = A::recip(o.h);  // executor.hpp:560-580
+        const double c = A::sqrt_(p.g * o.h);
+        double u, v;
+        A::div2(o.qx, o.qy, rc, u, v);
+        mx = fmax(mx, fabs(u) + c);
+        my = fmax(my, fabs(v) + c);
+        double* row = nxt + static_cast<size_t>(rr + R) * 3 * P + (i + R);
+        row[0] = o.h;
+        row[P] = o.qx;
+        row[2 * P] = o.qy;
+        if (!(xedge || jj == 0 || jj == p.ny - 1)) return;
+        if (i == 0) {
+            const CellVec g = edge_ghost(SWE_EDGE_W, p.bc[SWE_EDGE_W], o, p.z_w[rr + R], h_min);
+            row[-1] = g.h;
+            row[P - 1] = g.qx;
+            row[2 * P - 1] = g.qy;
+        }
+        if (i == p.nx - 1) {
+            const CellVec g = edge_ghost(SWE_EDGE_E, p.bc[SWE_EDGE_E], o, p.z_e[rr + R], h_min);
+            row[1] = g.h;
+            row[P + 1] = g.qx;
+            row[2 * P + 1] = g.qy;
+        }
+        if (jj == 0) {
+            const CellVec g = edge_ghost(SWE_EDGE_S, p.bc[SWE_EDGE_S], o, p.z_s[i], h_min);
+            double* gr = row - 3 * P;
+            gr[0] = g.h;
+            gr[P] = g.qx;
+            gr[2 * P] = g.qy;
+        }
+        if (jj == p.ny - 1) {
+            const CellVec g = edge_ghost(SWE_EDGE_N, p.bc[SWE_EDGE_N], o, p.z_n[i], h_min);
+            double* gr = row + 3 * P;
+            gr[0] = g.h;
+            gr[P] = g.qx;
+            gr[2 * P] = g.qy;
+        }
+    }
+
+    // boundary faces of row b (executor.hpp:471-514): walls carry pressure only,
+    // inflow the flux of the pump states, the other kinds use U* ghosts.
+    // Updates the own x face Hx and the y faces; returns the x face that belongs
+    // to the neighbouring out-of-domain lane (handed over by the caller).
+    __device__ __forceinline__ void boundary_faces(int b, int jb, const CellVec& U, const Flux& FU, const CellVec& Us,
+                                                const Flux& FS, CellVec& Hx, CellVec& hy_a, CellVec& hy_b,
+                                                CellVec& xo, int& give) {
+        give = 0;
+        if (!(i >= 0 && i < p.nx && jb >= 0 && jb < p.ny)) return;
+        const unsigned long long idx = static_cast<unsigned long long>(jb) * p.nx + i;
+        if (i == 0) {
+            const SweBC& bc = p.bc[SWE_EDGE_W];
+            CellVec w = Hx;
+            bool set = true;
+            if (bc.type == SWE_BC_WALL) {
+                w = {0.0, avg(FU.fxx, FS.fxx), 0.0};
+            } else if (bc.type == SWE_BC_INFLOW) {
+                const CellVec a = flux_x_plain(pump_state(SWE_EDGE_W, bc.q_n, U), half_g);
+                const CellVec c = flux_x_plain(pump_state(SWE_EDGE_W, bc.q_n, Us), half_g);
+                w = {avg(a.h, c.h), avg(a.qx, c.qx), avg(a.qy, c.qy)};
+            } else if (FWD) {
+                const CellVec g = edge_ghost(SWE_EDGE_W, bc, Us, p.z_w[b + R], h_min);
+                if (!(g.h >= h_min)) e4 = max(e4, ~idx);
+                const CellVec c = flux_x_plain(g, half_g);
+                w = {avg(U.qx, c.h), avg(FU.fxx, c.qx), avg(FU.fxy, c.qy)};
+            } else {
+                set = false;
+            }
+            if (set) {
+                if (FWD) { xo = w; give = 1; }  // the west face is lane t-1's
+                else Hx = w;
+            }
+        }
+        if (i == p.nx - 1) {
+            const SweBC& bc = p.bc[SWE_EDGE_E];
+            CellVec e = Hx;
+            bool set = true;
+            if (bc.type == SWE_BC_WALL) {
+                e = {0.0, avg(FU.fxx, FS.fxx), 0.0};
+            } else if (bc.type == SWE_BC_INFLOW) {
+                const CellVec a = flux_x_plain(pump_state(SWE_EDGE_E, bc.q_n, U), half_g);
+                const CellVec c = flux_x_plain(pump_state(SWE_EDGE_E, bc.q_n, Us), half_g);
+                e = {avg(a.h, c.h), avg(a.qx, c.qx), avg(a.qy, c.qy)};
+            } else if (!FWD) {
+                const CellVec g = edge_ghost(SWE_EDGE_E, bc, Us, p.z_e[b + R], h_min);
+                if (!(g.h >= h_min)) e4 = max(e4, ~idx);
+                const CellVec c = flux_x_plain(g, half_g);
+                e = {avg(U.qx, c.h), avg(FU.fxx, c.qx), avg(FU.fxy, c.qy)};
+            } else {
+                set = false;
+            }
+            if (set) {
+                if (FWD) Hx = e;
+                else { xo = e; give = 1; }  // the east face is lane t+1's
+            }
+        }
+        if (jb == 0) {
+            const SweBC& bc = p.bc[SWE_EDGE_S];
+            CellVec f = {0.0, 0.0, 0.0};
+            bool set = true;
+            if (bc.type == SWE_BC_WALL) {
+                f = {0.0, 0.0, avg(FU.gyy, FS.gyy)};
+            } else if (bc.type == SWE_BC_INFLOW) {
+                const CellVec a = flux_y_plain(pump_state(SWE_EDGE_S, bc.q_n, U), half_g);
+                const CellVec c = flux_y_plain(pump_state(SWE_EDGE_S, bc.q_n, Us), half_g);
+                f = {avg(a.h, c.h), avg(a.qx, c.qx), avg(a.qy, c.qy)};
+            } else if (FWD) {
+                const CellVec g = edge_ghost(SWE_EDGE_S, bc, Us, p.z_s[i], h_min);
+                if (!(g.h >= h_min)) e4 = max(e4, ~idx);
+                const CellVec c = flux_y_plain(g, half_g);
+                f = {avg(U.qy, c.h), avg(FU.fxy, c.qx), avg(FU.gyy, c.qy)};
+            } else {
+                set = false;
+            }
+            if (set) {
+                if (FWD) hy_a = f;
+                else hy_b = f;
+            }
+        }
+        if (jb == p.ny - 1) {
+            const SweBC& bc = p.bc[SWE_EDGE_N];
+            CellVec f = {0.0, 0.0, 0.0};
+            bool set = true;
+            if (bc.type == SWE_BC_WALL) {
+                f = {0.0, 0.0, avg(FU.gyy, FS.gyy)};
+            } else if (bc.type == SWE_BC_INFLOW) {
+                const CellVec a = flux_y_plain(pump_state(SWE_EDGE_N, bc.q_n, U), half_g);
+                const CellVec c = flux_y_plain(pump_state(SWE_EDGE_N, bc.q_n, Us), half_g);
+                f = {avg(a.h, c.h), avg(a.qx, c.qx), avg(a.qy, c.qy)};
+            } else if (!FWD) {
+                const CellVec g = edge_ghost(SWE_EDGE_N, bc, Us, p.z_n[i], h_min);
+                if (!(g.h >= h_min)) e4 = max(e4, ~idx);
+                const CellVec c = flux_y_plain(g, half_g);
+                f = {avg(U.qy, c.h), avg(FU.fxy, c.qx), avg(FU.gyy, c.qy)};
+            } else {
+                set = false;
+            }
+            if (set) {
+                if (FWD) hy_b = f;
+                else hy_a = f;
+            }
+        }
+    }
+
+    // One iteration k of the march: `in` -> `out`.
+    template <bool DO12, bool DO3, bool EMIT>
+    __device__ __forceinline__ void iter(int k, const Carry& in, Carry& out) {
+        const int b = r_start + S * k;  // stage-2 row (local)
+        if constexpr (DO12) {
+            // ======== stage 1: committed row b+S
+            consume(out.U, out.zx, out.zy);
+            const Rc rcN = A::recip(out.U.h);
+            out.FU = A::flux(out.U, rcN, half_g);
+            source_of<EXACT, MANNING>(out.U, out.FU, rcN, out.zx, out.zy, neg_g, gnn, out.srx, out.sry);
+
+            // ======== stage 2: predictor at (i, b)   scheme.hpp:100-113
+            const CellVec& U = in.U;
+            const Flux& FU = in.FU;
+            const CellVec& Un = out.U;
+            const Flux& FN = out.FU;
+            const double fn_h = shf_nb(U.qx);
+            const double fn_qx = shf_nb(FU.fxx);
+            const double fn_qy = shf_nb(FU.fxy);
+            double df_h, df_qx, df_qy, dg_h, dg_qx, dg_qy;
+            if constexpr (FWD) {
+                df_h = fn_h - U.qx; df_qx = fn_qx - FU.fxx; df_qy = fn_qy - FU.fxy;
+                dg_h = Un.qy - U.qy; dg_qx = FN.fxy - FU.fxy; dg_qy = FN.gyy - FU.gyy;
+            } else {
+                df_h = U.qx - fn_h; df_qx = FU.fxx - fn_qx; df_qy = FU.fxy - fn_qy;
+                dg_h = U.qy - Un.qy; dg_qx = FU.fxy - FN.fxy; dg_qy = FU.gyy - FN.gyy;
+            }
+            CellVec Us;
+            Us.h = (U.h - (dtdx * df_h + dtdy * dg_h)) + 0.0;
+            Us.qx = (U.qx - (dtdx * df_qx + dtdy * dg_qx)) + dt * in.srx;
+            Us.qy = (U.qy - (dtdx * df_qy + dtdy * dg_qy)) + dt * in.sry;
+
+            const int jb = p.j0 + b;
+            // dry U* -> row-major first consumer (executor.hpp:429-436, 459-513)
+            if (!(Us.h >= h_min) && star_ok && in_x && jb >= 0 && jb < p.ny) {
+                unsigned long long cons;
+                if (FWD) cons = static_cast<unsigned long long>(jb) * p.nx + i;
+                else if (jb >= 1) cons = static_cast<unsigned long long>(jb - 1) * p.nx + i;
+                else if (i >= 1) cons = static_cast<unsigned long long>(jb) * p.nx + (i - 1);
+                else cons = static_cast<unsigned long long>(jb) * p.nx + i;
+                e4 = max(e4, ~cons);
+            }
+            // K2 precondition on the committed state (scheme.hpp:35-39)
+            if (!(U.h >= h_min) && k >= 0 && k < L && out_x) e2 = 1;
+
+            const Rc rcS = A::recip(Us.h);
+            const Flux FS = A::flux(Us, rcS, half_g);
+            source_of<EXACT, MANNING>(Us, FS, rcS, in.zx, in.zy, neg_g, gnn, out.c_ssx, out.c_ssy);
+
+            // own x face (FWD: east, BWD: west) and y face (b, b+S)   scheme.hpp:153-161
+            CellVec Hx = {avg(fn_h, Us.qx), avg(fn_qx, FS.fxx), avg(fn_qy, FS.fxy)};
+            out.Hyp = {avg(Un.qy, Us.qy), avg(FN.fxy, FS.fxy), avg(FN.gyy, FS.gyy)};
+            CellVec hy_a = in.Hyp, hy_b = out.Hyp;  // faces (b-S, b) and (b, b+S)
+            if (xedge || jb == 0 || jb == p.ny - 1) {  // warp-uniform
+                CellVec xo = {0.0, 0.0, 0.0};
+                int give = 0;
+                boundary_faces(b, jb, U, FU, Us, FS, Hx, hy_a, hy_b, xo, give);
+                if (xedge) {  // hand the boundary face to the out-of-domain lane that owns it
+                    const double gh = shf_nb(xo.h), gqx = shf_nb(xo.qx), gqy = shf_nb(xo.qy);
+                    const int gv = FWD ? __shfl_down_sync(FULL, give, 1) : __shfl_up_sync(FULL, give, 1);
+                    if (gv && i == (FWD ? -1 : p.nx)) Hx = {gh, gqx, gqy};
+                }
+            }
+            out.c_hs = FWD ? hy_a : hy_b;
+            out.c_hn = FWD ? hy_b : hy_a;
+            out.c_hx = Hx;
+            out.Uc = U;
+            out.c_srx = in.srx;
+            out.c_sry = in.sry;
+        }
+
+        if constexpr (DO3) {
+            // ======== stage 3: corrector of row c = b - S   scheme.hpp:185-191
+            const CellVec ot = {shf_back(in.c_hx.h), shf_back(in.c_hx.qx), shf_back(in.c_hx.qy)};
+            const CellVec hw = FWD ? ot : in.c_hx, he = FWD ? in.c_hx : ot;
+            const double fs_h = dtdx * (he.h - hw.h) + dtdy * (in.c_hn.h - in.c_hs.h);
+            const double fs_qx = dtdx * (he.qx - hw.qx) + dtdy * (in.c_hn.qx - in.c_hs.qx);
+            const double fs_qy = dtdx * (he.qy - hw.qy) + dtdy * (in.c_hn.qy - in.c_hs.qy);
+            CellVec C;
+            C.h = (in.Uc.h - fs_h) + 0.0;
+            C.qx = (in.Uc.qx - fs_qx) + half_dt * (in.c_srx + in.c_ssx);
+            C.qy = (in.Uc.qy - fs_qy) + half_dt * (in.c_sry + in.c_ssy);
+            const int c_row = b - S;
+            if constexpr (!SMOOTH) {
+                if (EMIT && out_x) emit(C, c_row);
+            } else {
+                // smoothing of row q = c - S   (executor.hpp:533-540, scheme.hpp:197-204)
+                const CellVec& Cp = in.Cp;
+                if constexpr (EMIT) {
+                    CellVec ce = {__shfl_down_sync(FULL, Cp.h, 1), __shfl_down_sync(FULL, Cp.qx, 1),
+                                  __shfl_down_sync(FULL, Cp.qy, 1)};
+                    CellVec cw = {__shfl_up_sync(FULL, Cp.h, 1), __shfl_up_sync(FULL, Cp.qx, 1),
+                                  __shfl_up_sync(FULL, Cp.qy, 1)};
+                    if (out_x) {
+                        const int q = c_row - S;
+                        const int jq = p.j0 + q;
+                        CellVec cn = FWD ? C : in.Cpp;
+                        CellVec cs = FWD ? in.Cpp : C;
+                        if (xedge || jq == 0 || jq == p.ny - 1) {
+                            if (i == 0) cw = edge_ghost(SWE_EDGE_W, p.bc[SWE_EDGE_W], Cp, p.z_w[q + R], h_min);
+                            if (i == p.nx - 1) ce = edge_ghost(SWE_EDGE_E, p.bc[SWE_EDGE_E], Cp, p.z_e[q + R], h_min);
+                            if (jq == 0) cs = edge_ghost(SWE_EDGE_S, p.bc[SWE_EDGE_S], Cp, p.z_s[i], h_min);
+                            if (jq == p.ny - 1) cn = edge_ghost(SWE_EDGE_N, p.bc[SWE_EDGE_N], Cp, p.z_n[i], h_min);
+                        }
+                        const double nu = p.nu;
+                        CellVec o;
+                        o.h = Cp.h + nu * (((ce.h - Cp.h) + (cw.h - Cp.h)) + ((cn.h - Cp.h) + (cs.h - Cp.h)));
+                        o.qx = Cp.qx + nu * (((ce.qx - Cp.qx) + (cw.qx - Cp.qx)) + ((cn.qx - Cp.qx) + (cs.qx - Cp.qx)));
+                        o.qy = Cp.qy + nu * (((ce.qy - Cp.qy) + (cw.qy - Cp.qy)) + ((cn.qy - Cp.qy) + (cs.qy - Cp.qy)));
+                        emit(o, q);
+                    }
+                }
+                out.Cpp = Cp;
+                out.Cp = C;
+            }
+        }
+    }
+
+    // March one segment: output rows [ra, rb) of one 32-column window.
+    __device__ __forceinline__ void segment(const Seg& sg) {
+        L = sg.rb - sg.ra;
+        const int xw0 = sg.tile * TW - R;  // global column of lane 0
+        i = xw0 + lane;
+        in_x = (i >= 0) && (i < p.nx);
+        out_x = in_x && lane >= R && lane < 32 - R;
+        star_ok = FWD ? (lane < 31) : (lane > 0);
+        xedge = (xw0 <= 0) || (xw0 + 31 >= p.nx - 1);
+        r_start = FWD ? sg.ra : sg.rb - 1;
+
+        Carry A, B;
+        // pre-iteration: committed row r_start - S*R
+        consume(A.U, A.zx, A.zy);
+        {
+            const Rc rc = A::recip(A.U.h);
+            A.FU = A::flux(A.U, rc, half_g);
+            source_of<EXACT, MANNING>(A.U, A.FU, rc, A.zx, A.zy, neg_g, gnn, A.srx, A.sry);
+        }
+        A.Hyp = {0.0, 0.0, 0.0};
+        A.Cp = {0.0, 0.0, 0.0};
+        A.Cpp = {0.0, 0.0, 0.0};
+        int k;
+        if constexpr (!SMOOTH) {
+            // k = -1, 0: no corrector yet; 1..L-1 steady; L: corrector only
+            iter<true, false, false>(-1, A, B);
+            iter<true, false, false>(0, B, A);
+            k = 1;
+        } else {
+            // k = -2, -1: no corrector; 0, 1: corrector without output;
+            // 2..L steady; L+1: corrector + smoothing only
+            iter<true, false, false>(-2, A, B);
+            iter<true, false, false>(-1, B, A);
+            iter<true, true, false>(0, A, B);
+            iter<true, true, false>(1, B, A);
+            k = 2;
+        }
+        const int k_last = SMOOTH ? L : L - 1;  // last steady iteration
+        for (; k + 1 <= k_last; k += 2) {
+            iter<true, true, true>(k, A, B);
+            iter<true, true, true>(k + 1, B, A);
+        }
+        if (k <= k_last) {  // odd steady count
+            iter<true, true, true>(k, A, B);
+            iter<false, true, true>(k + 1, B, A);
+        } else {
+            iter<false, true, true>(k, A, B);
+        }
+    }
+};
+
+template <int WPB, bool FWD, bool SMOOTH, bool FLAT, bool MANNING, bool EXACT>
+__global__ void __launch_bounds__(WPB * 32, SWE_MINB) swe_step_kernel(const __grid_constant__ StepParams p) {
+    using M = Marcher<WPB, FWD, SMOOTH, FLAT, MANNING, EXACT>;
     constexpr int D = kStages;
-    constexpr int MAXSEG = 8;
+    constexpr int NF = M::NF;
+    constexpr unsigned FULL = 0xffffffffu;
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    double* stage = reinterpret_cast<double*>(smem_raw);  // [D][NF][NT]
-    double* xF = stage + D * NF * NT;                     // [2][3][NT] committed F (qx, fxx, fxy)
-    double* xH = xF + 2 * 3 * NT;                         // [2][3][NT] x-interface fluxes
-    double* xC = xH + 2 * 3 * NT;                         // [2][3][NT] corrector output (SMOOTH)
-    unsigned long long* bars =  // [D] full, [D] empty
-        reinterpret_cast<unsigned long long*>(xC + (SMOOTH ? 2 * 3 * NT : 0));
-    unsigned long long* ebars = bars + D;
-
-    __shared__ Seg segs[MAXSEG];
-    __shared__ int s_nseg, s_skip, s_sel, s_last;
-    __shared__ double s_dt, s_tc;
-    __shared__ double s_red[2][NT / 32];
-
     const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int lane = tid & 31;
+
+    __shared__ Seg segq_all[WPB][M::QN];
+    __shared__ int s_skip, s_sel, s_last;
+    __shared__ double s_dt, s_tc;
+    __shared__ double s_red[2][WPB];
     SweCtl* ctl = p.ctl;
+    double* stage = reinterpret_cast<double*>(smem_raw) + warp * (D * NF * 32);  // [D][NF][32]
+    unsigned long long* bars =
+        reinterpret_cast<unsigned long long*>(reinterpret_cast<double*>(smem_raw) + WPB * D * NF * 32) + warp * D;
 
     if (tid == 0) {
         const volatile SweCtl* vc = ctl;
@@ -202,379 +664,66 @@ __global__ void __launch_bounds__(NT + 32, 3) swe_step_kernel(const __grid_const
         s_dt = dt;
         s_tc = tc;
         s_sel = vc->sel;
-        s_nseg = seg_list(p, blockIdx.x, segs, MAXSEG);
-        for (int d = 0; d < D; ++d) {
-            mbar_init(&bars[d], 1);
-            mbar_init(&ebars[d], NT / 32);
-        }
+    }
+    if (lane == 0) {
+        for (int d = 0; d < D; ++d) mbar_init(&bars[d], 1);
         fence_mbar_init();
     }
     __syncthreads();
     if (s_skip) return;
 
-    const double dt = s_dt, tc = s_tc;
-    const double dtdx = dt / p.dx, dtdy = dt / p.dy, half_dt = 0.5 * dt;
-    const double* __restrict__ cur = p.buf[s_sel];
-    double* __restrict__ nxt = p.buf[s_sel ^ 1];
-    const int P = p.pitch;
-    const int nseg = s_nseg;
-    const double h_min = p.h_min, half_g = p.half_g, neg_g = p.neg_g, gnn = p.gnn;
-
-    int req = 0;  // next request to consume
-    double mx = 0.0, my = 0.0;
-    unsigned long long e2 = 0, e4 = 0, e5 = 0;
-
-    if (tid >= NT) {
-        // ---- producer warp: request n = (segment, row), L + 2R per segment, in
-        // consumption order; stage n % D is refilled once every compute warp
-        // has released request n - D (empty barrier).
-        if (tid == NT) {
-            int n = 0;
-            for (int k = 0; k < nseg; ++k) {
-                const int cnt = (segs[k].rb - segs[k].ra) + 2 * R;
-                const size_t col0 = static_cast<size_t>(segs[k].tile) * (NT - 2 * R);  // padded x0-R
-                for (int m = 0; m < cnt; ++m, ++n) {
-                    const int row = FWD ? segs[k].ra - R + m : segs[k].rb - 1 + R - m;
-                    const int d = n % D;
-                    if (n >= D) mbar_wait(&ebars[d], static_cast<unsigned>(((n / D) - 1) & 1));
-                    double* dst = stage + d * NF * NT;
-                    const double* src = cur + static_cast<size_t>(row + R) * 3 * P + col0;
-                    mbar_expect_tx(&bars[d], NF * NT * 8);
-                    bulk_g2s(dst, src, NT * 8, &bars[d]);
-                    bulk_g2s(dst + NT, src + P, NT * 8, &bars[d]);
-                    bulk_g2s(dst + 2 * NT, src + 2 * P, NT * 8, &bars[d]);
-                    if constexpr (!FLAT) {
-                        const double* ss = p.slope + static_cast<size_t>(row + R) * 2 * P + col0;
-                        bulk_g2s(dst + 3 * NT, ss, NT * 8, &bars[d]);
-                        bulk_g2s(dst + 4 * NT, ss + P, NT * 8, &bars[d]);
-                    }
-                }
-            }
-        }
-    } else {
-
-    const unsigned lane = tid & 31u;
-    auto consume = [&](CellVec& u, double& zx, double& zy) {
-        const int d = req % D;
-        mbar_wait(&bars[d], static_cast<unsigned>((req / D) & 1));
-        const double* st = stage + d * NF * NT;
-        u.h = st[tid];
-        u.qx = st[NT + tid];
-        u.qy = st[2 * NT + tid];
-        if constexpr (!FLAT) {
-            zx = st[3 * NT + tid];
-            zy = st[4 * NT + tid];
-        } else {
-            zx = 0.0;
-            zy = 0.0;
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&ebars[d]);
-    };
-    auto csync = [&]() { asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory"); };
-
-    for (int sgi = 0; sgi < nseg; ++sgi) {
-        const Seg sg = segs[sgi];
-        const int L = sg.rb - sg.ra;
-        const int i = sg.tile * (NT - 2 * R) - R + tid;  // global column of this thread
-        const bool in_x = (i >= 0) && (i < p.nx);
-        const bool out_x = in_x && tid >= R && tid < NT - R;
-        const bool corr_x = tid >= 1 && tid < NT - 1;
-        const bool star_ok = FWD ? (tid < NT - 1) : (tid > 0);
-        const int r_start = FWD ? sg.ra : sg.rb - 1;
-        // CTA-uniform: does this window touch the west/east domain edge?
-        const int xw0 = sg.tile * (NT - 2 * R) - R;
-        const bool xedge_cta = (xw0 <= 0) || (xw0 + NT - 1 >= p.nx - 1);
-        constexpr int E = R;             // warm-up rows
-        constexpr int X = SMOOTH ? 1 : 0;  // extra trailing iteration
-        constexpr int KC = SMOOTH ? -1 : 0;
-
-        // ---- pre-iteration: row r_start - S*E
-        CellVec U;
-        double zx, zy;
-        consume(U, zx, zy);
-        ++req;
-        Recip rcU = make_recip(U.h);
-        Flux FU = flux_of(U, rcU, half_g);
-        double srx, sry;
-        source_of<MANNING>(U, FU, rcU, zx, zy, neg_g, gnn, srx, sry);
-        int par = 0;
-        xF[(par * 3 + 0) * NT + tid] = U.qx;
-        xF[(par * 3 + 1) * NT + tid] = FU.fxx;
-        xF[(par * 3 + 2) * NT + tid] = FU.fxy;
-        csync();
-
-        CellVec Hyp = {0.0, 0.0, 0.0};
-        CellVec Cp = {0.0, 0.0, 0.0}, Cpp = {0.0, 0.0, 0.0};
-
-        for (int k = -E; k <= L - 1 + X; ++k) {
-            const int r = r_start + S * k;  // local row of this iteration
-            const int j = p.j0 + r;         // global row
-            // 1. lookahead row r+S
-            CellVec Un;
-            double zxn, zyn;
-            consume(Un, zxn, zyn);
-            ++req;
-            const Recip rcN = make_recip(Un.h);
-            const Flux FN = flux_of(Un, rcN, half_g);
-            double srxn, sryn;
-            source_of<MANNING>(Un, FN, rcN, zxn, zyn, neg_g, gnn, srxn, sryn);
-
-            // 2. predictor U* at (i, r)   scheme.hpp:100-113
-            const int tn = FWD ? (tid + 1 < NT ? tid + 1 : tid) : (tid > 0 ? tid - 1 : tid);
-            const double fn_h = xF[(par * 3 + 0) * NT + tn];
-            const double fn_qx = xF[(par * 3 + 1) * NT + tn];
-            const double fn_qy = xF[(par * 3 + 2) * NT + tn];
-            double df_h, df_qx, df_qy, dg_h, dg_qx, dg_qy;
-            if constexpr (FWD) {
-                df_h = fn_h - U.qx; df_qx = fn_qx - FU.fxx; df_qy = fn_qy - FU.fxy;
-                dg_h = Un.qy - U.qy; dg_qx = FN.fxy - FU.fxy; dg_qy = FN.gyy - FU.gyy;
-            } else {
-                df_h = U.qx - fn_h; df_qx = FU.fxx - fn_qx; df_qy = FU.fxy - fn_qy;
-                dg_h = U.qy - Un.qy; dg_qx = FU.fxy - FN.fxy; dg_qy = FU.gyy - FN.gyy;
-            }
-            CellVec Us;
-            Us.h = (U.h - (dtdx * df_h + dtdy * dg_h)) + 0.0;
-            Us.qx = (U.qx - (dtdx * df_qx + dtdy * dg_qx)) + dt * srx;
-            Us.qy = (U.qy - (dtdx * df_qy + dtdy * dg_qy)) + dt * sry;
-
-            // dry U* -> first consumer (executor.hpp:429-436, 459-513)
-            const bool row_in = (j >= 0) && (j < p.ny);
-            if (star_ok && in_x && row_in && !(Us.h >= h_min)) {
-                unsigned long long cons;
-                if (FWD) cons = static_cast<unsigned long long>(j) * p.nx + i;
-                else if (j >= 1) cons = static_cast<unsigned long long>(j - 1) * p.nx + i;
-                else if (i >= 1) cons = static_cast<unsigned long long>(j) * p.nx + (i - 1);
-                else cons = static_cast<unsigned long long>(j) * p.nx + i;
-                e4 = max(e4, ~cons);
-            }
-            const Recip rcS = make_recip(Us.h);
-            const Flux FS = flux_of(Us, rcS, half_g);
-            double ssx, ssy;
-            source_of<MANNING>(Us, FS, rcS, zx, zy, neg_g, gnn, ssx, ssy);
-
-            // 3. interface fluxes  scheme.hpp:153-161
-            CellVec Hxo;  // FWD: i+1/2 ; BWD: i-1/2
-            Hxo.h = 0.5 * (fn_h + Us.qx);
-            Hxo.qx = 0.5 * (fn_qx + FS.fxx);
-            Hxo.qy = 0.5 * (fn_qy + FS.fxy);
-            CellVec Hyn;  // FWD: j+1/2 ; BWD: j-1/2
-            Hyn.h = 0.5 * (Un.qy + Us.qy);
-            Hyn.qx = 0.5 * (FN.fxy + FS.fxy);
-            Hyn.qy = 0.5 * (FN.gyy + FS.gyy);
-            xH[(par * 3 + 0) * NT + tid] = Hxo.h;
-            xH[(par * 3 + 1) * NT + tid] = Hxo.qx;
-            xH[(par * 3 + 2) * NT + tid] = Hxo.qy;
-            xF[((par ^ 1) * 3 + 0) * NT + tid] = Un.qx;
-            xF[((par ^ 1) * 3 + 1) * NT + tid] = FN.fxx;
-            xF[((par ^ 1) * 3 + 2) * NT + tid] = FN.fxy;
-            csync();
-
-            // 4. corrector  executor.hpp:451-519, scheme.hpp:185-191
-            CellVec C = {0.0, 0.0, 0.0};
-            const bool do_corr = (k >= KC) && corr_x;
-            if (do_corr) {
-                const int to = tid - S;
-                CellVec Hxx;
-                Hxx.h = xH[(par * 3 + 0) * NT + to];
-                Hxx.qx = xH[(par * 3 + 1) * NT + to];
-                Hxx.qy = xH[(par * 3 + 2) * NT + to];
-                CellVec hw = FWD ? Hxx : Hxo, he = FWD ? Hxo : Hxx;
-                CellVec hs = FWD ? Hyp : Hyn, hn = FWD ? Hyn : Hyp;
-                const bool yedge_row = (j == 0) || (j == p.ny - 1);
-                if ((xedge_cta || yedge_row) && in_x && row_in) {
-                    const bool west = (i == 0), east = (i == p.nx - 1);
-                    const bool south = (j == 0), north = (j == p.ny - 1);
-                    if (west | east | south | north) {
-                        const unsigned long long idx = static_cast<unsigned long long>(j) * p.nx + i;
-                        if (west) {
-                            const SweBC& bc = p.bc[SWE_EDGE_W];
-                            if (bc.type == SWE_BC_WALL) {
-                                hw = {0.0, 0.5 * (FU.fxx + FS.fxx), 0.0};
-                            } else if (bc.type == SWE_BC_INFLOW) {
-                                const CellVec a = flux_x_plain(pump_state(SWE_EDGE_W, bc.q_n, U), half_g);
-                                const CellVec b = flux_x_plain(pump_state(SWE_EDGE_W, bc.q_n, Us), half_g);
-                                hw = {0.5 * (a.h + b.h), 0.5 * (a.qx + b.qx), 0.5 * (a.qy + b.qy)};
-                            } else if (FWD) {
-                                const CellVec g = edge_ghost(SWE_EDGE_W, bc, Us, p.z_w[r + R], h_min);
-                                if (!(g.h >= h_min)) e4 = max(e4, ~idx);
-                                const CellVec b = flux_x_plain(g, half_g);
-                                hw = {0.5 * (U.qx + b.h), 0.5 * (FU.fxx + b.qx), 0.5 * (FU.fxy + b.qy)};
-                            }
-                        }
-                        if (east) {
-                            const SweBC& bc = p.bc[SWE_EDGE_E];
-                            if (bc.type == SWE_BC_WALL) {
-                                he = {0.0, 0.5 * (FU.fxx + FS.fxx), 0.0};
-                            } else if (bc.type == SWE_BC_INFLOW) {
-                                const CellVec a = flux_x_plain(pump_state(SWE_EDGE_E, bc.q_n, U), half_g);
-                                const CellVec b = flux_x_plain(pump_state(SWE_EDGE_E, bc.q_n, Us), half_g);
-                                he = {0.5 * (a.h + b.h), 0.5 * (a.qx + b.qx), 0.5 * (a.qy + b.qy)};
-                            } else if (!FWD) {
-                                const CellVec g = edge_ghost(SWE_EDGE_E, bc, Us, p.z_e[r + R], h_min);
-                                if (!(g.h >= h_min)) e4 = max(e4, ~idx);
-                                const CellVec b = flux_x_plain(g, half_g);
-                                he = {0.5 * (U.qx + b.h), 0.5 * (FU.fxx + b.qx), 0.5 * (FU.fxy + b.qy)};
-                            }
-                        }
-                        if (south) {
-                            const SweBC& bc = p.bc[SWE_EDGE_S];
-                            if (bc.type == SWE_BC_WALL) {
-                                hs = {0.0, 0.0, 0.5 * (FU.gyy + FS.gyy)};
-                            } else if (bc.type == SWE_BC_INFLOW) {
-                                const CellVec a = flux_y_plain(pump_state(SWE_EDGE_S, bc.q_n, U), half_g);
-                                const CellVec b = flux_y_plain(pump_state(SWE_EDGE_S, bc.q_n, Us), half_g);
-                                hs = {0.5 * (a.h + b.h), 0.5 * (a.qx + b.qx), 0.5 * (a.qy + b.qy)};
-                            } else if (FWD) {
-                                const CellVec g = edge_ghost(SWE_EDGE_S, bc, Us, p.z_s[i], h_min);
-                                if (!(g.h >= h_min)) e4 = max(e4, ~idx);
-                                const CellVec b = flux_y_plain(g, half_g);
-                                hs = {0.5 * (U.qy + b.h), 0.5 * (FU.fxy + b.qx), 0.5 * (FU.gyy + b.qy)};
-                            }
-                        }
-                        if (north) {
-                            const SweBC& bc = p.bc[SWE_EDGE_N];
-                            if (bc.type == SWE_BC_WALL) {
-                                hn = {0.0, 0.0, 0.5 * (FU.gyy + FS.gyy)};
-                            } else if (bc.type == SWE_BC_INFLOW) {
-                                const CellVec a = flux_y_plain(pump_state(SWE_EDGE_N, bc.q_n, U), half_g);
-                                const CellVec b = flux_y_plain(pump_state(SWE_EDGE_N, bc.q_n, Us), half_g);
-                                hn = {0.5 * (a.h + b.h), 0.5 * (a.qx + b.qx), 0.5 * (a.qy + b.qy)};
-                            } else if (!FWD) {
-                                const CellVec g = edge_ghost(SWE_EDGE_N, bc, Us, p.z_n[i], h_min);
-                                if (!(g.h >= h_min)) e4 = max(e4, ~idx);
-                                const CellVec b = flux_y_plain(g, half_g);
-                                hn = {0.5 * (U.qy + b.h), 0.5 * (FU.fxy + b.qx), 0.5 * (FU.gyy + b.qy)};
-                            }
-                        }
-                    }
-                }
-                const double fs_h = dtdx * (he.h - hw.h) + dtdy * (hn.h - hs.h);
-                const double fs_qx = dtdx * (he.qx - hw.qx) + dtdy * (hn.qx - hs.qx);
-                const double fs_qy = dtdx * (he.qy - hw.qy) + dtdy * (hn.qy - hs.qy);
-                C.h = (U.h - fs_h) + 0.0;
-                C.qx = (U.qx - fs_qx) + half_dt * (srx + ssx);
-                C.qy = (U.qy - fs_qy) + half_dt * (sry + ssy);
-            }
-
-            // K2 precondition on the committed state (scheme.hpp:35-39)
-            if (k >= 0 && k < L && out_x && !(U.h >= h_min)) e2 = 1;
-
-            // 5. output row (guard, CFL, store, next-step ghosts)
-            auto emit = [&](const CellVec& o, int rr) {
-                const int jj = p.j0 + rr;
-                const unsigned long long idx = static_cast<unsigned long long>(jj) * p.nx + i;
-                const bool ok = finite_d(o.h) && finite_d(o.qx) && finite_d(o.qy) && o.h >= h_min;
-                if (!ok) e5 = max(e5, ~idx);
-                // K6 executor.hpp:560-580
-                const Recip rc = make_recip(o.h);
-                const double c = __dsqrt_rn(p.g * o.h);
-                double u, v;
-                div2(o.qx, o.qy, rc, u, v);
-                const double sx = fabs(u) + c;
-                const double sy = fabs(v) + c;
-                mx = fmax(mx, sx);
-                my = fmax(my, sy);
-                const size_t rb = static_cast<size_t>(rr + R) * 3;
-                const size_t col = static_cast<size_t>(i + R);
-                nxt[(rb + 0) * P + col] = o.h;
-                nxt[(rb + 1) * P + col] = o.qx;
-                nxt[(rb + 2) * P + col] = o.qy;
-                // K1 of the next step: ghosts of the committed candidate
-                if (!(xedge_cta || jj == 0 || jj == p.ny - 1)) return;
-                if (i == 0) {
-                    const CellVec g = edge_ghost(SWE_EDGE_W, p.bc[SWE_EDGE_W], o, p.z_w[rr + R], h_min);
-                    nxt[(rb + 0) * P + col - 1] = g.h;
-                    nxt[(rb + 1) * P + col - 1] = g.qx;
-                    nxt[(rb + 2) * P + col - 1] = g.qy;
-                }
-                if (i == p.nx - 1) {
-                    const CellVec g = edge_ghost(SWE_EDGE_E, p.bc[SWE_EDGE_E], o, p.z_e[rr + R], h_min);
-                    nxt[(rb + 0) * P + col + 1] = g.h;
-                    nxt[(rb + 1) * P + col + 1] = g.qx;
-                    nxt[(rb + 2) * P + col + 1] = g.qy;
-                }
-                if (jj == 0) {
-                    const CellVec g = edge_ghost(SWE_EDGE_S, p.bc[SWE_EDGE_S], o, p.z_s[i], h_min);
-                    const size_t gb = static_cast<size_t>(rr - 1 + R) * 3;
-                    nxt[(gb + 0) * P + col] = g.h;
-                    nxt[(gb + 1) * P + col] = g.qx;
-                    nxt[(gb + 2) * P + col] = g.qy;
-                }
-                if (jj == p.ny - 1) {
-                    const CellVec g = edge_ghost(SWE_EDGE_N, p.bc[SWE_EDGE_N], o, p.z_n[i], h_min);
-                    const size_t gb = static_cast<size_t>(rr + 1 + R) * 3;
-                    nxt[(gb + 0) * P + col] = g.h;
-                    nxt[(gb + 1) * P + col] = g.qx;
-                    nxt[(gb + 2) * P + col] = g.qy;
-                }
-            };
-
-            if constexpr (!SMOOTH) {
-                if (k >= 0 && out_x) emit(C, r);
-            } else {
-                // smoothing of row q = r - S   (executor.hpp:533-540, scheme.hpp:197-204)
-                if (k >= 1 && out_x) {
-                    const int q = r - S;
-                    const int jq = p.j0 + q;
-                    const int pp = par ^ 1;
-                    CellVec Ce, Cw, Cn, Cs;
-                    Ce = {xC[(pp * 3 + 0) * NT + tid + 1], xC[(pp * 3 + 1) * NT + tid + 1],
-                          xC[(pp * 3 + 2) * NT + tid + 1]};
-                    Cw = {xC[(pp * 3 + 0) * NT + tid - 1], xC[(pp * 3 + 1) * NT + tid - 1],
-                          xC[(pp * 3 + 2) * NT + tid - 1]};
-                    Cn = FWD ? C : Cpp;
-                    Cs = FWD ? Cpp : C;
-                    if (xedge_cta || jq == 0 || jq == p.ny - 1) {
-                    if (i == 0) Cw = edge_ghost(SWE_EDGE_W, p.bc[SWE_EDGE_W], Cp, p.z_w[q + R], h_min);
-                    if (i == p.nx - 1) Ce = edge_ghost(SWE_EDGE_E, p.bc[SWE_EDGE_E], Cp, p.z_e[q + R], h_min);
-                    if (jq == 0) Cs = edge_ghost(SWE_EDGE_S, p.bc[SWE_EDGE_S], Cp, p.z_s[i], h_min);
-                    if (jq == p.ny - 1) Cn = edge_ghost(SWE_EDGE_N, p.bc[SWE_EDGE_N], Cp, p.z_n[i], h_min);
-                    }
-                    const double nu = p.nu;
-                    CellVec o;
-                    o.h = Cp.h + nu * (((Ce.h - Cp.h) + (Cw.h - Cp.h)) + ((Cn.h - Cp.h) + (Cs.h - Cp.h)));
-                    o.qx = Cp.qx + nu * (((Ce.qx - Cp.qx) + (Cw.qx - Cp.qx)) + ((Cn.qx - Cp.qx) + (Cs.qx - Cp.qx)));
-                    o.qy = Cp.qy + nu * (((Ce.qy - Cp.qy) + (Cw.qy - Cp.qy)) + ((Cn.qy - Cp.qy) + (Cs.qy - Cp.qy)));
-                    emit(o, q);
-                }
-                xC[(par * 3 + 0) * NT + tid] = C.h;
-                xC[(par * 3 + 1) * NT + tid] = C.qx;
-                xC[(par * 3 + 2) * NT + tid] = C.qy;
-                Cpp = Cp;
-                Cp = C;
-            }
-
-            // 6. shift the march
-            U = Un;
-            FU = FN;
-            srx = srxn;
-            sry = sryn;
-            zx = zxn;
-            zy = zyn;
-            Hyp = Hyn;
-            par ^= 1;
-        }
-        csync();  // smem exchange slots are reused by the next segment
+    M m{p};
+    m.stage = stage;
+    m.bars = bars;
+    m.segq = segq_all[warp];
+    m.qhead = 0;
+    m.qtail = 0;
+    m.lane = lane;
+    m.cur = p.buf[s_sel];
+    m.nxt = p.buf[s_sel ^ 1];
+    m.P = p.pitch;
+    m.dt = s_dt;
+    m.dtdx = m.dt / p.dx;  // scheme.hpp:110, 188-190
+    m.dtdy = m.dt / p.dy;
+    m.half_dt = 0.5 * m.dt;
+    m.h_min = p.h_min;
+    m.half_g = p.half_g;
+    m.neg_g = p.neg_g;
+    m.gnn = p.gnn;
+    m.pleft = 0;
+    m.pdone = false;
+    m.psrc = nullptr;
+    m.pstep = 0;
+    m.pn = 0;
+    m.req = 0;
+    m.ring = {0, 0u};
+    m.mx = 0.0;
+    m.my = 0.0;
+    m.e2 = m.e4 = m.e5 = 0ull;
+    m.produce();
+    while (m.qhead < m.qtail) {  // the producer keeps the queue ahead of the consumer
+        const Seg sg = m.segq[m.qhead % M::QN];
+        ++m.qhead;
+        m.segment(sg);
     }
-    }  // compute threads
 
     // ---- CTA reduction of the CFL maxima and error words
+    double mx = m.mx, my = m.my;
     for (int o = 16; o > 0; o >>= 1) {
-        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        my = fmax(my, __shfl_xor_sync(0xffffffffu, my, o));
+        mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
+        my = fmax(my, __shfl_xor_sync(FULL, my, o));
     }
-    if ((tid & 31) == 0 && tid < NT) {
-        s_red[0][tid >> 5] = mx;
-        s_red[1][tid >> 5] = my;
+    if (lane == 0) {
+        s_red[0][warp] = mx;
+        s_red[1][warp] = my;
     }
-    if (e2) atomicMax(&ctl->red[RED_E2], 1ull);
-    if (e4) atomicMax(&ctl->red[RED_E4], e4);
-    if (e5) atomicMax(&ctl->red[RED_E5], e5);
+    if (m.e2) atomicMax(&ctl->red[RED_E2], 1ull);
+    if (m.e4) atomicMax(&ctl->red[RED_E4], m.e4);
+    if (m.e5) atomicMax(&ctl->red[RED_E5], m.e5);
     __syncthreads();
     if (tid == 0) {
         double a = s_red[0][0], b = s_red[1][0];
-        for (int w = 1; w < NT / 32; ++w) {
+        for (int w = 1; w < WPB; ++w) {
             a = fmax(a, s_red[0][w]);
             b = fmax(b, s_red[1][w]);
         }
@@ -591,14 +740,13 @@ __global__ void __launch_bounds__(NT + 32, 3) swe_step_kernel(const __grid_const
     __syncthreads();
     if (s_last && tid == 0) {
         __threadfence();
-        finalize_step(p, ctl, dt, tc);
+        finalize_step(p, ctl, s_dt, s_tc);
     }
 }
 
-template <int NT, bool FWD, bool SMOOTH, bool FLAT>
+template <int WPB, bool SMOOTH, bool FLAT>
 constexpr size_t step_smem_bytes() {
-    return static_cast<size_t>(kStages) * (FLAT ? 3 : 5) * NT * 8 + 2 * 3 * NT * 8 * (SMOOTH ? 3 : 2) +
-           2 * kStages * 8;
+    return static_cast<size_t>(WPB) * kStages * (FLAT ? 3 : 5) * 32 * 8 + WPB * kStages * 8;
 }
 
 }  // namespace swe_dev

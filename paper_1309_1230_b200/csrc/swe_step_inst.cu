@@ -1,20 +1,29 @@
 // swe_step_inst.cu — instantiations of the fused step kernel and a launcher
 // table indexed by (sweep parity, smoothing, flat bed, Manning friction).
-// Compiled with -fmad=false: the expression trees must not be contracted
-// (parity contract with the reference built with -ffp-contract=off).
+//
+// Compiled twice (see __graft_entry__.build):
+//   SWE_EXACT_TU=1 with -fmad=false: expression trees are never contracted, so
+//     the step is bit-identical to the reference built with -ffp-contract=off;
+//   SWE_EXACT_TU=0 with -fmad=true: FMA contraction + shared reciprocals
+//     (tolerance parity).
 #include <cstdio>
 
 #include "swe_launch.h"
 #include "swe_step.cuh"
 
+#ifndef SWE_EXACT_TU
+#define SWE_EXACT_TU 1
+#endif
+
 namespace {
 
-constexpr int kNT = SWE_STEP_NT;
+constexpr int kWPB = SWE_STEP_WPB;  // warps (independent workers) per CTA
+constexpr bool kExact = SWE_EXACT_TU != 0;
 
 template <bool FWD, bool SMOOTH, bool FLAT, bool MANNING>
 cudaError_t launch_one(int grid, cudaStream_t s, const StepParams& p) {
-    constexpr size_t smem = swe_dev::step_smem_bytes<kNT, FWD, SMOOTH, FLAT>();
-    auto k = swe_dev::swe_step_kernel<kNT, FWD, SMOOTH, FLAT, MANNING>;
+    constexpr size_t smem = swe_dev::step_smem_bytes<kWPB, SMOOTH, FLAT>();
+    auto k = swe_dev::swe_step_kernel<kWPB, FWD, SMOOTH, FLAT, MANNING, kExact>;
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -22,28 +31,28 @@ cudaError_t launch_one(int grid, cudaStream_t s, const StepParams& p) {
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    k<<<grid, kNT + 32, smem, s>>>(p);
+    k<<<grid, kWPB * 32, smem, s>>>(p);
     return cudaGetLastError();
 }
 
 template <bool FWD, bool SMOOTH, bool FLAT, bool MANNING>
 int occupancy_one() {
-    constexpr size_t smem = swe_dev::step_smem_bytes<kNT, FWD, SMOOTH, FLAT>();
-    auto k = swe_dev::swe_step_kernel<kNT, FWD, SMOOTH, FLAT, MANNING>;
+    constexpr size_t smem = swe_dev::step_smem_bytes<kWPB, SMOOTH, FLAT>();
+    auto k = swe_dev::swe_step_kernel<kWPB, FWD, SMOOTH, FLAT, MANNING, kExact>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kNT + 32, smem) != cudaSuccess) return 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kWPB * 32, smem) != cudaSuccess) return 1;
     return n > 0 ? n : 1;
 }
 
 using LaunchFn = cudaError_t (*)(int, cudaStream_t, const StepParams&);
 using OccFn = int (*)();
 
-#define SWE_V(F, S, Z, M) {launch_one<F, S, Z, M>, occupancy_one<F, S, Z, M>}
 struct Entry {
     LaunchFn launch;
     OccFn occ;
 };
+#define SWE_V(F, S, Z, M) {launch_one<F, S, Z, M>, occupancy_one<F, S, Z, M>}
 const Entry kTable[16] = {
     SWE_V(false, false, false, false), SWE_V(false, false, false, true),
     SWE_V(false, false, true, false),  SWE_V(false, false, true, true),
@@ -58,18 +67,13 @@ const Entry kTable[16] = {
 
 }  // namespace
 
-int swe_step_variant(bool fwd, bool smooth, bool flat, bool manning) {
-    return (fwd ? 8 : 0) | (smooth ? 4 : 0) | (flat ? 2 : 0) | (manning ? 1 : 0);
-}
-
-cudaError_t swe_launch_step(int variant, int grid, cudaStream_t stream, const StepParams& p) {
+#if SWE_EXACT_TU
+cudaError_t swe_launch_step_exact(int variant, int grid, cudaStream_t stream, const StepParams& p) {
     return kTable[variant & 15].launch(grid, stream, p);
 }
+int swe_step_occupancy_exact(int variant) { return kTable[variant & 15].occ(); }
 
-int swe_step_occupancy(int variant) { return kTable[variant & 15].occ(); }
-
-__global__ void swe_finalize_kernel(const __grid_constant__ StepParams p, int fwd_unused) {
-    (void)fwd_unused;
+__global__ void swe_finalize_kernel(const __grid_constant__ StepParams p) {
     SweCtl* c = p.ctl;
     const volatile SweCtl* vc = c;
     if (vc->done) return;
@@ -89,6 +93,12 @@ __global__ void swe_finalize_kernel(const __grid_constant__ StepParams p, int fw
 }
 
 cudaError_t swe_launch_finalize(cudaStream_t stream, const StepParams& p) {
-    swe_finalize_kernel<<<1, 1, 0, stream>>>(p, 0);
+    swe_finalize_kernel<<<1, 1, 0, stream>>>(p);
     return cudaGetLastError();
 }
+#else
+cudaError_t swe_launch_step_fast(int variant, int grid, cudaStream_t stream, const StepParams& p) {
+    return kTable[variant & 15].launch(grid, stream, p);
+}
+int swe_step_occupancy_fast(int variant) { return kTable[variant & 15].occ(); }
+#endif

@@ -49,6 +49,7 @@ struct __align__(16) SweCtl {
     int err_kind;                 // 2/4/5/6: which plan kernel raised
     int err_i, err_j;
     unsigned int finish;          // CTA arrival counter for the last-block finalize
+    unsigned int work;            // dynamic work-item counter of the step kernel
     unsigned long long red[RED_N];
 };
 
@@ -68,6 +69,8 @@ struct StepParams {
     int pitch;             // doubles per field row (P)
     int ntiles;            // x tiles
     int ncta;              // CTAs launched
+    int chunk;             // rows per dynamic work item
+    int nchunks;           // row chunks per tile (items = ntiles * nchunks)
     int finalize;          // 1: last CTA finalizes (one rank); 0: host-side allreduce + finalize kernel
     int nranks;
     double dx, dy, g, half_g, neg_g, gnn, h_min, nu;

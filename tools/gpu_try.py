@@ -44,3 +44,18 @@ fs = five_drops(40); sc = gen_square_dam(40); run("mixed40", sc.spec, sc.phys, s
 sc = gen_square_dam(1024); g = Stepper(sc.spec, sc.phys, sc.pol, sc.bounds); g.load(sc.build())
 t0 = time.time(); res = g.advance(1e18, 0, math.nan, 1000); el = time.time()-t0
 print("advance 1024^2 x1000", res, el, "cells/s", 1024*1024*1000/el)
+
+# fast mode tolerance probe
+def run_fast(name, sc, fs, steps):
+    g = Stepper(sc.spec, sc.phys, sc.pol, sc.bounds, ExecutorKind(exact=False))
+    r = OracleStepper(sc.spec, sc.phys, sc.pol, sc.bounds)
+    g.load(fs); r.load(fs)
+    dg = g.compute_dt(math.inf); dr = r.compute_dt(math.inf)
+    for k in range(steps):
+        dg = g.step(dg, k).dt_next; dr = r.step(dr, k).dt_next
+    a, b = g.state(), r.state()
+    ua, ub = a.qx / a.h, b.qx / b.h; va, vb = a.qy / a.h, b.qy / b.h
+    print("FAST", name, steps, "max|dh|", np.abs(a.h - b.h).max(), "max|du|", np.abs(ua - ub).max(), "max|dv|", np.abs(va - vb).max(), "dt rel", abs(dg - dr) / dr)
+sc = gen_square_dam(256); run_fast("dam256", sc, sc.build(), 1000)
+sc = gen_square_dam(48); run_fast("drops48", sc, five_drops(48), 200)
+sc = gen_channel_flood(128); run_fast("chan128man", sc, sc.build(), 500)
