@@ -15,6 +15,7 @@
 #include <string>
 #include <vector>
 
+#include <cudaTypedefs.h>
 #include <nccl.h>
 
 #include "swe_device.cuh"
@@ -195,6 +196,34 @@ __global__ void scan_kernel(const double* b, int P, int R, int nx, int nloc, int
         if (minr) atomicMax(&out[SCAN_MINR], minr);
         if (guard) atomicMax(&out[SCAN_GUARD], guard);
     }
+}
+
+// ---------------------------------------------------------------- TMA descriptors
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+bool encode_rows(CUtensorMap* map, double* base, int P, long long field_rows, int box_rows, std::string& err) {
+    if (!g_encode) {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn) {
+            err = "cuTensorMapEncodeTiled unavailable";
+            return false;
+        }
+        g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(P), static_cast<cuuint64_t>(field_rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(P) * sizeof(double)};
+    const cuuint32_t box[2] = {32u, static_cast<cuuint32_t>(box_rows)};
+    const cuuint32_t estr[2] = {1u, 1u};
+    const CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, base, dims, strides, box, estr,
+                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        err = "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")";
+        return false;
+    }
+    return true;
 }
 
 // ---------------------------------------------------------------- helpers
@@ -666,6 +695,12 @@ EXPORT int swe_cuda_create(const swe_grid* grid, const swe_physics* phys, const 
     }
 
     StepParams& p = c->prm;
+    {
+        std::string err;
+        for (int k = 0; k < 2; ++k)
+            if (!encode_rows(&p.tmap_state[k], c->d_buf[k], c->pitch, static_cast<long long>(rows) * 3, 3, err))
+                return set_status(st, SWE_ERR_RUNTIME, -1, -1, 0, "%s", err.c_str());
+    }
     p.buf[0] = c->d_buf[0];
     p.buf[1] = c->d_buf[1];
     p.slope = nullptr;
@@ -794,6 +829,11 @@ EXPORT int swe_cuda_load(swe_ctx* c, const double* z, const double* h, const dou
     cudaFree(d_zp);
     c->flat = (flag == 0);
     c->prm.slope = c->d_slope;
+    {
+        std::string err;
+        if (!encode_rows(&c->prm.tmap_slope, c->d_slope, P, static_cast<long long>(nloc + 2 * R) * 2, 2, err))
+            return set_status(st, SWE_ERR_RUNTIME, -1, -1, 0, "%s", err.c_str());
+    }
 
     // K1 ghosts of the committed state + strip halos
     const int gthreads = std::max(nloc, nx);

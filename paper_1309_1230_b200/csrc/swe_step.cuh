@@ -73,6 +73,28 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
         : "memory");
 }
 
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,
+                                            unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+            "r"(smem_u32(dst)),
+        "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+#ifndef SWE_LOADER
+#define SWE_LOADER 2  // 0: 1D bulk copies; 1: per-lane cp.async (LDGSTS); 2: 2D TMA tensor maps
+#endif
+
 // ------------------------------------------------------------ work partition
 // Worker w (one warp) owns units [w*U/G, (w+1)*U/G) of the unit space
 // u = tile*nloc + row.  A unit run is split into segments at tile boundaries.
@@ -215,6 +237,8 @@ struct Marcher {
     int pleft;
     bool pdone;
     const double* psrc;
+    const double* pzsrc;
+    int px, py, sel;  // TMA tensor coordinates of the next request; committed buffer
     long long pstep;
     int pn, req;
     WarpRing ring;
@@ -259,32 +283,66 @@ struct Marcher {
         pleft = (sg.rb - sg.ra) + 2 * R;
         const int row = FWD ? sg.ra - R : sg.rb - 1 + R;
         const size_t col0 = static_cast<size_t>(sg.tile) * TW;  // padded offset of x0-R
-        if (lane < 3) {
-            psrc = cur + (static_cast<size_t>(row + R) * 3 + lane) * P + col0;
-            pstep = static_cast<long long>(S) * 3 * P;
+        if constexpr (SWE_LOADER == 2) {
+            px = static_cast<int>(col0);
+            py = (row + R) * 3;
+        } else if constexpr (SWE_LOADER == 0) {
+            if (lane < 3) {
+                psrc = cur + (static_cast<size_t>(row + R) * 3 + lane) * P + col0;
+                pstep = static_cast<long long>(S) * 3 * P;
+            } else {
+                psrc = p.slope + (static_cast<size_t>(row + R) * 2 + (lane - 3)) * P + col0;
+                pstep = static_cast<long long>(S) * 2 * P;
+            }
         } else {
-            psrc = p.slope + (static_cast<size_t>(row + R) * 2 + (lane - 3)) * P + col0;
-            pstep = static_cast<long long>(S) * 2 * P;
+            psrc = cur + static_cast<size_t>(row + R) * 3 * P + col0 + lane;
+            pstep = static_cast<long long>(S) * 3 * P;
+            if constexpr (!FLAT) pzsrc = p.slope + static_cast<size_t>(row + R) * 2 * P + col0 + lane;
         }
     }
     __device__ __forceinline__ void produce() {
         while (pn < req + D - 1) {
+            if (pleft == 0 && !(pdone || qtail - qhead >= QN - 1)) prod_seg();
             if (pleft == 0) {
-                if (pdone || qtail - qhead >= QN - 1) return;
-                prod_seg();
-                if (pleft == 0) return;
+                if constexpr (SWE_LOADER == 1) {  // keep one commit group per request slot
+                    cp_async_commit();
+                    ++pn;
+                    continue;
+                }
+                return;
             }
             const int d = pn % D;
-            if (lane == 0) mbar_expect_tx(&bars[d], NF * 32 * 8);
-            __syncwarp();
-            if (lane < NF) bulk_g2s(stage + (d * NF + lane) * 32, psrc, 32 * 8, &bars[d]);
-            psrc += pstep;
+            if constexpr (SWE_LOADER == 2) {
+                if (lane == 0) {
+                    mbar_expect_tx(&bars[d], NF * 32 * 8);
+                    tma_load_2d(stage + d * NF * 32, &p.tmap_state[sel], px, py, &bars[d]);
+                    if constexpr (!FLAT) tma_load_2d(stage + d * NF * 32 + 96, &p.tmap_slope, px, (py / 3) * 2, &bars[d]);
+                }
+                py += S * 3;
+            } else if constexpr (SWE_LOADER == 0) {
+                if (lane == 0) mbar_expect_tx(&bars[d], NF * 32 * 8);
+                __syncwarp();
+                if (lane < NF) bulk_g2s(stage + (d * NF + lane) * 32, psrc, 32 * 8, &bars[d]);
+            } else {
+                double* dst = stage + d * NF * 32 + lane;
+                cp_async8(dst, psrc);
+                cp_async8(dst + 32, psrc + P);
+                cp_async8(dst + 64, psrc + 2 * P);
+                if constexpr (!FLAT) {
+                    cp_async8(dst + 96, pzsrc);
+                    cp_async8(dst + 128, pzsrc + P);
+                    pzsrc += static_cast<long long>(S) * 2 * P;
+                }
+                cp_async_commit();
+            }
+            if constexpr (SWE_LOADER != 2) psrc += pstep;
             --pleft;
             ++pn;
         }
     }
     __device__ __forceinline__ void consume(CellVec& u, double& zx, double& zy) {
-        mbar_wait(&bars[ring.d], ring.ph);
+        if constexpr (SWE_LOADER != 1) mbar_wait(&bars[ring.d], ring.ph);
+        else cp_async_wait<D - 2>();  // groups are committed one per request slot
         const double* st = stage + ring.d * NF * 32;
         u.h = st[lane];
         u.qx = st[32 + lane];
@@ -680,6 +738,9 @@ __global__ void __launch_bounds__(WPB * 32, SWE_MINB) swe_step_kernel(const __gr
     m.qtail = 0;
     m.lane = lane;
     m.cur = p.buf[s_sel];
+    m.sel = s_sel;
+    m.px = 0;
+    m.py = 0;
     m.nxt = p.buf[s_sel ^ 1];
     m.P = p.pitch;
     m.dt = s_dt;
@@ -692,6 +753,7 @@ __global__ void __launch_bounds__(WPB * 32, SWE_MINB) swe_step_kernel(const __gr
     m.gnn = p.gnn;
     m.pleft = 0;
     m.pdone = false;
+    m.pzsrc = nullptr;
     m.psrc = nullptr;
     m.pstep = 0;
     m.pn = 0;

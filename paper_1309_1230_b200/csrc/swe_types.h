@@ -4,6 +4,8 @@
 
 #include <cstdint>
 
+#include <cuda.h>
+
 #include "../../include/swe_cuda.h"
 
 enum { SWE_EDGE_N = 0, SWE_EDGE_S = 1, SWE_EDGE_E = 2, SWE_EDGE_W = 3 };
@@ -57,6 +59,10 @@ struct __align__(16) SweCtl {
 
 // Kernel parameters (passed by value as a __grid_constant__).
 struct StepParams {
+    // 2D TMA descriptors: state buffer k viewed as [3*(nloc+2R) field rows][P]
+    // (box 32 x 3 = h, qx, qy of one row); slopes as [2*(nloc+2R)][P] (box 32 x 2)
+    CUtensorMap tmap_state[2];
+    CUtensorMap tmap_slope;
     double* buf[2];        // committed/candidate state, row-interleaved SoA
     const double* slope;   // dzdx/dzdy rows, same layout; nullptr for a flat bed
     const double* z_w;     // bed z at i=0 per local row
