@@ -198,6 +198,14 @@ int32_t swe_cuda_halo_rows(const swe_ctx* ctx);
 /* ncclGetUniqueId into out[SWE_NCCL_ID_BYTES] (rank 0 broadcasts it). */
 int swe_cuda_nccl_unique_id(void* out, swe_status* st);
 
+/* ---- diagnostics ----------------------------------------------------- */
+/* Runs the step kernel's shared-reciprocal division on device arrays copied
+ * from the host: out[k] = a[k] / b[k] as the step computes it (exact != 0:
+ * SWE_EXEC_EXACT arithmetic, else the fast-mode quotient).  Used by the
+ * parity tests to prove the exact path equals IEEE division. */
+int swe_cuda_selftest_div(const double* a, const double* b, size_t n, int exact, double* out,
+                          swe_status* st);
+
 /* ---- misc ------------------------------------------------------------ */
 const char* swe_cuda_version(void);
 /* Number of step-kernel launches issued since create (bench evidence). */

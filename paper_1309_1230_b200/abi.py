@@ -100,6 +100,7 @@ SIGNATURES = {
     "swe_cuda_nccl_unique_id": (C.c_int, [C.c_void_p, ST]),
     "swe_cuda_version": (C.c_char_p, []),
     "swe_cuda_launch_count": (C.c_uint64, [C.c_void_p]),
+    "swe_cuda_selftest_div": (C.c_int, [DP, DP, C.c_size_t, C.c_int, DP, ST]),
 }
 
 _lib = None

@@ -226,6 +226,20 @@ bool encode_rows(CUtensorMap* map, double* base, int P, long long field_rows, in
     return true;
 }
 
+// Shared-reciprocal division of the step kernels (swe_device.cuh), exposed for
+// the parity self-test.  Compiled with -fmad=false like the exact kernels.
+__global__ void selftest_div_kernel(const double* a, const double* b, size_t n, int exact, double* out) {
+    for (size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; k < n;
+         k += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        if (exact) {
+            const swe_dev::Recip rc = swe_dev::make_recip(b[k]);
+            out[k] = swe_dev::div_rn(a[k], rc);
+        } else {
+            out[k] = a[k] * swe_dev::make_recip_fast(b[k]).y;
+        }
+    }
+}
+
 // ---------------------------------------------------------------- helpers
 double std_min(double a, double b) { return (b < a) ? b : a; }
 
@@ -1128,6 +1142,23 @@ EXPORT int swe_cuda_advance(swe_ctx* c, double t_end, uint64_t step_index0, doub
     res->guard_warnings = static_cast<int32_t>(warn * h.steps_done);
     c->warnings_total += res->guard_warnings;
     if (rc_final) return rc_final;
+    return ok_status(st);
+}
+
+EXPORT int swe_cuda_selftest_div(const double* a, const double* b, size_t n, int exact, double* out,
+                                  swe_status* st) {
+    double *da = nullptr, *db = nullptr, *dout = nullptr;
+    CUDA_TRY(cudaMalloc(&da, n * 8 + 8));
+    CUDA_TRY(cudaMalloc(&db, n * 8 + 8));
+    CUDA_TRY(cudaMalloc(&dout, n * 8 + 8));
+    CUDA_TRY(cudaMemcpy(da, a, n * 8, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(db, b, n * 8, cudaMemcpyHostToDevice));
+    selftest_div_kernel<<<148 * 8, 256>>>(da, db, n, exact, dout);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpy(out, dout, n * 8, cudaMemcpyDeviceToHost));
+    cudaFree(da);
+    cudaFree(db);
+    cudaFree(dout);
     return ok_status(st);
 }
 

@@ -1,0 +1,274 @@
+"""GPU parity: libswe_cuda.so against the CPU oracle and the reference goldens.
+
+Exact mode (SWE_EXEC_EXACT, -fmad=false) must be bit-identical to the
+reference on every case without Manning friction (std::pow is not
+bit-reproducible on CUDA).  Fast mode (FMA + shared
+reciprocals) must agree within the stated tolerance:
+    max |dh|, |du|, |dv| <= FAST_TOL after the case's steps.
+All calls go through the C-ABI (ctypes mirror in paper_1309_1230_b200/stepper.py).
+"""
+import math
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from golden_cases import bits_equal, cases
+from oracle import oracle as O
+from paper_1309_1230_b200 import scenarios as S
+from paper_1309_1230_b200 import abi
+from paper_1309_1230_b200.stepper import (BoundaryKind, BoundarySet, ConfigError, ExecutorKind, FieldSet, GridSpec,
+                                          InstabilityError, PhysicsParams, StabilityPolicy, Stepper)
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+FAST_TOL = 1e-10   # absolute, on h, u = qx/h, v = qy/h (O(1) fields); measured ~1e-14
+MANNING_TOL = 1e-12
+CASES = cases()
+EXACT = ExecutorKind(exact=True)
+FAST = ExecutorKind(exact=False)
+
+
+def uv(fs_h, fs_qx, fs_qy):
+    return fs_qx / fs_h, fs_qy / fs_h
+
+
+def max_err(a_h, a_qx, a_qy, b_h, b_qx, b_qy):
+    ua, va = uv(a_h, a_qx, a_qy)
+    ub, vb = uv(b_h, b_qx, b_qy)
+    return max(np.abs(a_h - b_h).max(), np.abs(ua - ub).max(), np.abs(va - vb).max())
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c.name for c in CASES])
+def test_exact_mode_matches_reference_golden(case):
+    st = Stepper(case.spec, case.phys, case.pol, case.bounds, EXACT)
+    fin, err, dt_next, warnings = case.run(st)
+    exp = case.expected_error()
+    if case.manning:  # pow(h, 4/3): tolerance-only
+        assert err == exp
+        assert max_err(fin.h, fin.qx, fin.qy, case.h, case.qx, case.qy) <= MANNING_TOL
+        return
+    assert err == exp, (err, exp)
+    assert bits_equal(fin.h, case.h) and bits_equal(fin.qx, case.qx) and bits_equal(fin.qy, case.qy)
+    assert fin.t == case.meta["t_final"]
+    if err is None:
+        assert dt_next == case.meta["dt_next"]
+        assert warnings == case.meta["warnings"]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c.name for c in CASES])
+def test_fast_mode_within_tolerance(case):
+    st = Stepper(case.spec, case.phys, case.pol, case.bounds, FAST)
+    fin, err, dt_next, warnings = case.run(st)
+    exp = case.expected_error()
+    if exp is None:
+        assert err is None
+        assert max_err(fin.h, fin.qx, fin.qy, case.h, case.qx, case.qy) <= FAST_TOL
+        assert abs(dt_next - case.meta["dt_next"]) <= 1e-12 * case.meta["dt_next"]
+    else:
+        assert err is not None and err[1] == exp[1]
+
+
+def test_shared_reciprocal_division_is_ieee():
+    rng = np.random.Generator(np.random.PCG64(7))
+    n = 1 << 22
+    a = rng.standard_normal(n) * np.exp2(rng.integers(-60, 60, n))
+    b = np.abs(rng.standard_normal(n)) * np.exp2(rng.integers(-60, 60, n)) + 1e-300
+    special = np.array([0.0, -0.0, 1e-320, -1e-320, 5e-324, 1e300, -1e300, 1.7e308, np.inf, -np.inf, np.nan,
+                        2.2250738585072014e-308, 1.0, -1.0, 3.0, 1e-308, 4.9e-310])
+    sa, sb = np.meshgrid(special, np.concatenate([special, [0.5, 2.0, 1e-10, 1e10, 7.0]]))
+    a = np.concatenate([a, sa.ravel(), (a[:1000] * 0.0)])
+    b = np.concatenate([b, sb.ravel(), b[:1000]])
+    out = np.empty_like(a)
+    st = abi.swe_status()
+    lib = abi.load_library()
+    assert lib.swe_cuda_selftest_div(abi.dptr(a), abi.dptr(b), a.size, 1, abi.dptr(out), st) == 0
+    with np.errstate(all="ignore"):
+        ref = a / b
+    same = (out.view(np.uint64) == ref.view(np.uint64)) | (np.isnan(out) & np.isnan(ref))
+    assert same.all(), (a[~same][:5], b[~same][:5], out[~same][:5], ref[~same][:5])
+
+
+def test_step_equals_device_resident_advance():
+    sc = S.gen_square_dam(200)
+    fs = sc.build()
+    for kind in (EXACT, FAST):
+        a = Stepper(sc.spec, sc.phys, sc.pol, sc.bounds, kind)
+        b = Stepper(sc.spec, sc.phys, sc.pol, sc.bounds, kind)
+        a.load(fs)
+        b.load(fs)
+        dt = a.compute_dt(math.inf)
+        for k in range(150):
+            dt = a.step(dt, k).dt_next
+        r = b.advance(1e18, 0, math.nan, 150)
+        assert r.steps == 150 and r.step_index == 150 and r.dt_next == dt
+        x, y = a.state(), b.state()
+        assert x.t == y.t
+        assert bits_equal(x.h, y.h) and bits_equal(x.qx, y.qx) and bits_equal(x.qy, y.qy)
+
+
+def test_advance_lands_on_t_end_like_run_from():
+    # run.hpp:149-163: identical to driving the oracle with the same loop
+    sc = S.gen_square_dam(64)
+    g = Stepper(sc.spec, sc.phys, sc.pol, sc.bounds, EXACT)
+    o = O.OracleStepper(sc.spec, sc.phys, sc.pol, sc.bounds)
+    g.load(sc.build())
+    o.load(sc.build())
+    rg = g.advance(7.3)
+    ro = o.advance(7.3)
+    assert rg.t_final == 7.3 == ro.t_final
+    assert (rg.steps, rg.step_index, rg.dt_next) == (ro.steps, ro.step_index, ro.dt_next)
+    a, b = g.state(), o.state()
+    assert bits_equal(a.h, b.h) and bits_equal(a.qx, b.qx)
+    # resume (odd parity origin, given first dt) continues bit-identically
+    rg2 = g.advance(9.0, rg.step_index, rg.dt_next)
+    ro2 = o.advance(9.0, ro.step_index, ro.dt_next)
+    assert (rg2.steps, rg2.t_final, rg2.dt_next) == (ro2.steps, ro2.t_final, ro2.dt_next)
+    assert bits_equal(g.state().h, o.state().h)
+
+
+def test_failure_is_atomic_and_located_like_the_oracle():
+    sc = S.gen_dam_break(48, 1.0, 1e-4)
+    phys = PhysicsParams(nu_art=0.0)
+    g = Stepper(sc.spec, phys, sc.pol, sc.bounds, EXACT)
+    o = O.OracleStepper(sc.spec, phys, sc.pol, sc.bounds)
+    g.load(sc.build())
+    o.load(sc.build())
+    dg, do = g.compute_dt(1e9), o.compute_dt(1e9)
+    assert dg == do
+    for k in range(200):
+        before = g.state()
+        try:
+            rg = g.step(dg, k)
+        except InstabilityError as e:
+            with pytest.raises(InstabilityError) as eo:
+                o.step(do, k)
+            assert (e.cell_i(), e.cell_j(), e.sim_time()) == (eo.value.cell_i(), eo.value.cell_j(),
+                                                              eo.value.sim_time())
+            assert e.cell_i() >= 0 and e.cell_j() >= 0 and e.sim_time() > 0.0
+            after = g.state()
+            assert bits_equal(after.h, before.h) and after.t == before.t  # failure atomicity
+            return
+        ro = o.step(do, k)
+        assert rg.dt_next == ro.dt_next
+        dg, do = rg.dt_next, ro.dt_next
+    pytest.fail("engineered dry shelf did not fail")
+
+
+def test_guard_error_reports_first_offender_and_values():
+    spec = GridSpec(20, 16, 1.0, 1.0)
+    fs = S.flat_pool(spec, 1.0)
+    fs.qx[9, 13] = math.nan
+    fs.qx[12, 2] = math.nan
+    g = Stepper(spec, PhysicsParams(), StabilityPolicy(cfl=0.45), BoundarySet.all(BoundaryKind.wall()), EXACT)
+    g.load(fs)
+    with pytest.raises(InstabilityError) as e:
+        g.guard()
+    assert (e.value.cell_i(), e.value.cell_j()) == (13, 9)
+    with pytest.raises(InstabilityError) as e2:
+        g.step(0.1, 0)
+    o = O.OracleStepper(spec, PhysicsParams(), StabilityPolicy(cfl=0.45), BoundarySet.all(BoundaryKind.wall()))
+    o.load(fs)
+    with pytest.raises(InstabilityError) as e3:
+        o.step(0.1, 0)
+    assert (e2.value.cell_i(), e2.value.cell_j(), e2.value.sim_time()) == \
+        (e3.value.cell_i(), e3.value.cell_j(), e3.value.sim_time())
+    # NaN momentum poisons the predicted depth next door: the corrector (K4) raises
+    # before the guard (K5), exactly as in the reference's plan order
+    assert str(e2.value).startswith("predicted depth")
+
+
+def test_config_errors():
+    with pytest.raises(ConfigError):
+        Stepper(GridSpec(8, 8), PhysicsParams(nu_art=0.7), StabilityPolicy(), BoundarySet())
+    st = Stepper(GridSpec(8, 8), PhysicsParams(), StabilityPolicy(), BoundarySet())
+    with pytest.raises(ConfigError):
+        st.step(0.1, 0)  # no state loaded
+    st.load(S.flat_pool(GridSpec(8, 8), 1.0))
+    with pytest.raises(ConfigError):
+        st.step(math.inf, 0)
+
+
+def test_still_water_fixed_point_full_size():
+    # test_executor.cpp:118-133 at the BASELINE size: bit-exact fixed point incl. signbit
+    spec = GridSpec(8192, 8192, 1.0, 1.0)
+    g = Stepper(spec, PhysicsParams(), StabilityPolicy(cfl=0.45), BoundarySet.all(BoundaryKind.wall()), EXACT)
+    fs = S.flat_pool(spec, 1.0)
+    g.load(fs)
+    r = g.advance(1e18, 0, math.nan, 20)
+    assert r.steps == 20
+    out = g.state()
+    assert (out.h == 1.0).all()
+    assert (out.qx.view(np.uint64) == 0).all() and (out.qy.view(np.uint64) == 0).all()
+
+
+def test_closed_box_conserves_volume_full_size():
+    # validate.hpp:145-165: closed-box drift <= 1e-11 (reference measures ~1e-15)
+    sc = S.gen_square_dam(8192)
+    g = Stepper(sc.spec, sc.phys, sc.pol, sc.bounds, FAST)
+    fs = sc.build()
+    v0 = math.fsum(fs.h.ravel())
+    g.load(fs)
+    g.advance(1e18, 0, math.nan, 50)
+    v1 = math.fsum(g.state().h.ravel())
+    assert abs(v1 - v0) / v0 <= 1e-11
+
+
+def test_transpose_symmetry_large():
+    # test_executor.cpp:377-416 on a 1536 x 1024 random state, both parities, exact mode
+    rng = np.random.Generator(np.random.PCG64(31))
+    a = FieldSet(GridSpec(1536, 1024, 1.0, 1.0))
+    a.h[:] = rng.uniform(0.8, 1.4, a.h.shape)
+    a.qx[:] = rng.uniform(-0.2, 0.2, a.h.shape)
+    a.qy[:] = rng.uniform(-0.2, 0.2, a.h.shape)
+    b = FieldSet(GridSpec(1024, 1536, 1.0, 1.0), None, a.h.T.copy(), a.qy.T.copy(), a.qx.T.copy())
+    walls = BoundarySet.all(BoundaryKind.wall())
+    pol = StabilityPolicy(cfl=0.45)
+    for par in (0, 1):
+        ga = Stepper(a.spec, PhysicsParams(), pol, walls, EXACT)
+        gb = Stepper(b.spec, PhysicsParams(), pol, walls, EXACT)
+        ga.load(a)
+        gb.load(b)
+        dt = 0.5 * ga.compute_dt(1e9)
+        ga.step(dt, par)
+        gb.step(dt, par)
+        x, y = ga.state(), gb.state()
+        assert bits_equal(x.h, y.h.T) and bits_equal(x.qx, y.qy.T) and bits_equal(x.qy, y.qx.T)
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+def test_full_size_c3_frictionless_against_reference():
+    # BASELINE config 3 at 8192^2 (frictionless variant): 2 steps vs the reference decomposed:N
+    sc = S.gen_channel_flood(8192, manning_n=0.0)
+    fs = sc.build()
+    g = Stepper(sc.spec, sc.phys, sc.pol, sc.bounds, EXACT)
+    g.load(fs)
+    r = O.RefStepper(sc.spec, sc.phys, sc.pol, sc.bounds, O.REF_DECOMPOSED, os.cpu_count() or 1)
+    r.load(fs)
+    dg, dr = g.compute_dt(math.inf), r.compute_dt(math.inf, os.cpu_count() or 1)
+    assert dg == dr
+    for k in range(2):
+        dg = g.step(dg, k).dt_next
+        dr = r.step(dr, k).dt_next
+        assert dg == dr
+    x, y = g.state(), r.state()
+    assert bits_equal(x.h, y.h) and bits_equal(x.qx, y.qx) and bits_equal(x.qy, y.qy)
+
+
+def test_cpp_shim():
+    exe = os.path.join(ROOT, "build", "shim_test")
+    assert os.path.exists(exe), "run __graft_entry__.build()"
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "OK" in r.stdout
+
+
+def test_launch_count_is_one_kernel_per_step():
+    sc = S.gen_square_dam(512)
+    g = Stepper(sc.spec, sc.phys, sc.pol, sc.bounds, EXACT)
+    g.load(sc.build())
+    n0 = g.launch_count()
+    g.advance(1e18, 0, math.nan, 128)
+    assert g.launch_count() - n0 == 128
