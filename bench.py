@@ -34,6 +34,7 @@ CONFIGS = {
     "c3": "8192x8192 synthetic channel flood (gen_channel_flood(8192), Manning 0.035), HBM-roofline benchmark",
     "c3f": "8192x8192 channel flood, frictionless variant (manning_n = 0; bit-exact parity config)",
     "c1": "256x256 square dam break (h_l 1.0, h_r 0.5, walls)",
+    "d8k": "8192x8192 square dam break (flat bed; 48 B/cell), roofline probe",
     "c2": "512x512 square dam break (interactive size)",
     "c4": "32768x32768 square dam break (row strips)",
     "c5": "16384x16384 mostly-dry floodplain dam break (split_x = n/8, h_r = 1e-3, nu_art = 0.05)",
@@ -59,6 +60,8 @@ def scenario_for(cfg: str, nranks: int):
         return sc, 56  # algorithmic bytes/cell-step: read h,qx,qy,z + write h,qx,qy (fp64)
     if cfg == "c1":
         return S.gen_square_dam(256), 48
+    if cfg == "d8k":
+        return S.gen_square_dam(8192), 48
     if cfg == "c2":
         return S.gen_square_dam(512), 48
     if cfg == "c4":
