@@ -74,7 +74,7 @@ NcclApi g_nccl;
 using swe_dev::CellVec;
 
 __device__ __forceinline__ size_t pidx(int P, int R, int lr, int f, int i) {
-    return (static_cast<size_t>(lr + R) * 3 + f) * P + static_cast<size_t>(i + SWE_XOFF);
+    return (static_cast<size_t>(lr + R) * 3 + f) * P + static_cast<size_t>(i + R);
 }
 
 // Fill the whole padded buffer (every field row, all columns) with a benign
@@ -153,8 +153,8 @@ __global__ void slopes_kernel(const double* zp, double* slope, int P, int R, int
             sy = (zat(i, jn) - zat(i, js)) / two_dy;
             if (swe_dev::dbits(sx) != 0ull || swe_dev::dbits(sy) != 0ull) atomicOr(flags, 1u);
         }
-        slope[(static_cast<size_t>(lr + R) * 2 + 0) * P + (i + SWE_XOFF)] = sx;
-        slope[(static_cast<size_t>(lr + R) * 2 + 1) * P + (i + SWE_XOFF)] = sy;
+        slope[(static_cast<size_t>(lr + R) * 2 + 0) * P + (i + R)] = sx;
+        slope[(static_cast<size_t>(lr + R) * 2 + 1) * P + (i + R)] = sy;
     }
 }
 
@@ -201,8 +201,7 @@ __global__ void scan_kernel(const double* b, int P, int R, int nx, int nloc, int
 // ---------------------------------------------------------------- TMA descriptors
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
-bool encode_rows(CUtensorMap* map, double* base, int P, long long field_rows, int box_rows, std::string& err,
-                 int box_cols = SWE_WIN) {
+bool encode_rows(CUtensorMap* map, double* base, int P, long long field_rows, int box_rows, std::string& err) {
     if (!g_encode) {
         cudaDriverEntryPointQueryResult q;
         void* fn = nullptr;
@@ -215,7 +214,7 @@ bool encode_rows(CUtensorMap* map, double* base, int P, long long field_rows, in
     }
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(P), static_cast<cuuint64_t>(field_rows)};
     const cuuint64_t strides[1] = {static_cast<cuuint64_t>(P) * sizeof(double)};
-    const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
+    const cuuint32_t box[2] = {32u, static_cast<cuuint32_t>(box_rows)};
     const cuuint32_t estr[2] = {1u, 1u};
     const CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, base, dims, strides, box, estr,
                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -496,7 +495,7 @@ void cell_values(swe_ctx* c, int which, unsigned long long idx, double* h, doubl
     if (lr < 0 || lr >= c->nloc) return;
     double v[3];
     for (int f = 0; f < 3; ++f)
-        cudaMemcpy(&v[f], c->d_buf[which] + (static_cast<size_t>(lr + c->R) * 3 + f) * c->pitch + (i + SWE_XOFF), 8,
+        cudaMemcpy(&v[f], c->d_buf[which] + (static_cast<size_t>(lr + c->R) * 3 + f) * c->pitch + (i + c->R), 8,
                    cudaMemcpyDeviceToHost);
     *h = v[0];
     *qx = v[1];
@@ -659,9 +658,9 @@ EXPORT int swe_cuda_create(const swe_grid* grid, const swe_physics* phys, const 
     c->R = c->smooth ? 2 : 1;
     c->j0 = bands[ex.rank].first;
     c->nloc = bands[ex.rank].second - bands[ex.rank].first;
-    const int out_w = SWE_TILE_W;
+    const int out_w = SWE_TILE_W(c->R);
     c->ntiles = (grid->nx + out_w - 1) / out_w;
-    c->pitch = ((c->ntiles * out_w + 2 * SWE_XOFF) + 31) / 32 * 32;  // last window ends at ntiles*TW + 4
+    c->pitch = ((c->ntiles * out_w + 2 * c->R + 32) + 31) / 32 * 32;
     const size_t rows = static_cast<size_t>(c->nloc + 2 * c->R);
     c->buf_doubles = rows * 3 * c->pitch;
     *out = c;
@@ -712,13 +711,9 @@ EXPORT int swe_cuda_create(const swe_grid* grid, const swe_physics* phys, const 
     StepParams& p = c->prm;
     {
         std::string err;
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < 2; ++k)
             if (!encode_rows(&p.tmap_state[k], c->d_buf[k], c->pitch, static_cast<long long>(rows) * 3, 3, err))
                 return set_status(st, SWE_ERR_RUNTIME, -1, -1, 0, "%s", err.c_str());
-            if (!encode_rows(&p.tmap_out[k], c->d_buf[k], c->pitch, static_cast<long long>(rows) * 3, 3, err,
-                             out_w))
-                return set_status(st, SWE_ERR_RUNTIME, -1, -1, 0, "%s", err.c_str());
-        }
     }
     p.buf[0] = c->d_buf[0];
     p.buf[1] = c->d_buf[1];
@@ -790,7 +785,7 @@ EXPORT int swe_cuda_load(swe_ctx* c, const double* z, const double* h, const dou
     c->sel = 0;
     const double* src[3] = {h, qx, qy};
     for (int f = 0; f < 3; ++f) {
-        double* dst = c->d_buf[0] + (static_cast<size_t>(R) * 3 + f) * P + SWE_XOFF;
+        double* dst = c->d_buf[0] + (static_cast<size_t>(R) * 3 + f) * P + R;
         CUDA_TRY(cudaMemcpy2DAsync(dst, 3 * P * sizeof(double), src[f], rowb, rowb, nloc,
                                    cudaMemcpyHostToDevice, c->stream));
     }
@@ -935,7 +930,7 @@ EXPORT int swe_cuda_state(swe_ctx* c, double* z, double* h, double* qx, double* 
     double* dst[3] = {h, qx, qy};
     for (int f = 0; f < 3; ++f) {
         if (!dst[f]) continue;
-        const double* src = c->d_buf[c->sel] + (static_cast<size_t>(R) * 3 + f) * P + SWE_XOFF;
+        const double* src = c->d_buf[c->sel] + (static_cast<size_t>(R) * 3 + f) * P + R;
         CUDA_TRY(cudaMemcpy2DAsync(dst[f], rowb, src, 3 * P * sizeof(double), rowb, c->nloc,
                                    cudaMemcpyDeviceToHost, c->stream));
     }

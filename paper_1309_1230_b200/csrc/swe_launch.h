@@ -9,8 +9,7 @@
 #ifndef SWE_STEP_WPB
 #define SWE_STEP_WPB 4   // warps per CTA; every warp is an independent row-march worker
 #endif
-#define SWE_WIN 64                         // columns per warp window (two per lane)
-#define SWE_TILE_W (SWE_WIN - 2 * SWE_XOFF)  // output columns per window
+#define SWE_TILE_W(R) (32 - 2 * (R))  // output columns per warp window
 
 inline int swe_step_variant(bool fwd, bool smooth, bool flat, bool manning) {
     return (fwd ? 8 : 0) | (smooth ? 4 : 0) | (flat ? 2 : 0) | (manning ? 1 : 0);

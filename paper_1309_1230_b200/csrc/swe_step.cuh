@@ -1,27 +1,215 @@
-// swe_step.cuh — the fused MacCormack step (plan K1-K6 + smoothing) as one
-// sm_100a kernel per time step.  Every lane owns TWO adjacent columns, a
-// warp a 64-column window (2 halo + 60 output + 2 halo columns).  Same numerics and plan as swe_step.cuh (merged
-// schedule: stage 1 load+fluxes of row b+S, stage 2 predictor of row b,
-// stage 3 corrector/smoothing/guard/CFL/store), but the per-row costs of a
-// lane (ring wait, TMA issue, bookkeeping, votes, row addressing) are shared
-// by two cells, the x exchange needs one shuffle per pair instead of one per
-// cell, and the two cells give the scheduler independent dependency chains.
+// swe_step.cuh — the fused MacCormack step (plan kernels K1-K6 + smoothing)
+// as ONE sm_100a kernel per time step.
+//
+// Reference plan (executor.hpp:113-148, naive strategy 846-911):
+//   K1 ghost fill (committed) -> K2 predictor -> K3 ghost fill (U*) ->
+//   K4 corrector [+ ghost fill + 5-point smoothing] -> K5 guard -> K6 CFL min.
+// Here:
+//   K1   ghosts of the committed state are written by the previous step's
+//        epilogue (or the load kernel) into the padded buffer, so the
+//        predictor reads them as ordinary cells.
+//   K2+K4 fused per warp with row marching: a warp owns a 32-column window
+//        (30 output columns, 28 with smoothing) and walks a contiguous run of
+//        rows in the sweep direction, independently of every other warp (no
+//        CTA barriers).  Each state's fluxes F/G are evaluated once per cell
+//        and shared: x-neighbours through warp shuffles, y-neighbours in
+//        registers.  Interface fluxes
+//        H_{i+1/2} are evaluated once per interface (the reference computes
+//        them twice, bit-identically: README.md:191-196).
+//   K3   U* ghosts are formed in-thread at domain edges only.
+//   K5/K6 fused into the epilogue: guard offenders and dry-U* consumers go to
+//        atomicMax(~index) words (row-major first offender wins); the CFL
+//        reduction keeps max sx / max sy because min_k RN(dx/sx_k) =
+//        RN(dx / max_k sx_k) (correctly rounded division is monotone).
+//   Finalize: the last CTA to finish turns the reduction words into
+//        StepResult / errors and commits by flipping the ping-pong selector
+//        in the device control block (executor.hpp:836-840).
+// Committed rows arrive through a per-warp cp.async.bulk (TMA bulk copy)
+// ring with mbarrier completion; stores are coalesced 8-byte STG.
 #pragma once
 
-#include "swe_common.cuh"
+#include "swe_device.cuh"
 
 namespace swe_dev {
 
-// Registers carried from one row to the next.  The committed state and bed
-// slopes of row b are NOT carried: they are re-read from row b's TMA ring slot,
-// which is only refilled at the end of the iteration that consumes row b+S.
-// The source term is recomputed from them (carried only with Manning friction,
-// whose pow/rcbrt is too expensive to repeat).
+constexpr int kStages = 5;
+#ifndef SWE_MINB
+#define SWE_MINB 3
+#endif
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,
+                                            unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+            "r"(smem_u32(dst)),
+        "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+#ifndef SWE_LOADER
+#define SWE_LOADER 2  // 0: 1D bulk copies; 1: per-lane cp.async (LDGSTS); 2: 2D TMA tensor maps
+#endif
+
+// ------------------------------------------------------------ work partition
+// Worker w (one warp) owns units [w*U/G, (w+1)*U/G) of the unit space
+// u = tile*nloc + row.  A unit run is split into segments at tile boundaries.
+struct Seg {
+    int tile, ra, rb;
+};
+
+__device__ __forceinline__ int seg_list(const StepParams& p, long long w, long long nw, Seg* segs,
+                                        int maxseg) {
+    const long long total = static_cast<long long>(p.ntiles) * p.nloc;
+    long long u = total * w / nw;
+    const long long u1 = total * (w + 1) / nw;
+    int n = 0;
+    while (u < u1 && n < maxseg) {
+        const int tile = static_cast<int>(u / p.nloc);
+        const int ra = static_cast<int>(u % p.nloc);
+        const long long left = u1 - u;
+        const int rb = static_cast<int>(left < (p.nloc - ra) ? ra + left : p.nloc);
+        segs[n++] = {tile, ra, rb};
+        u += rb - ra;
+    }
+    return n;
+}
+
+// --------------------------------------------------------------- finalize
+// executor.hpp:889-903 (K5/K6 outcome) + 1091-1104 (finish_dt) + 836-840 (commit).
+__device__ __forceinline__ void finalize_step(const StepParams& p, SweCtl* c, double dt, double tc) {
+    volatile unsigned long long* red = c->red;
+    const unsigned long long e2 = red[RED_E2], e4 = red[RED_E4], e5 = red[RED_E5];
+    const unsigned long long dg = red[RED_DIAG];
+    const double msx = __longlong_as_double(static_cast<long long>(red[RED_SX]));
+    const double msy = __longlong_as_double(static_cast<long long>(red[RED_SY]));
+    int status = 0, kind = 0, ei = -1, ej = -1;
+    double et = 0.0, edt = 0.0, dt_next = 0.0;
+    if (e2) {
+        status = SWE_ERR_INSTABILITY; kind = 2;
+    } else if (e4) {
+        const unsigned long long idx = ~e4;
+        status = SWE_ERR_INSTABILITY; kind = 4;
+        ei = static_cast<int>(idx % static_cast<unsigned long long>(p.nx));
+        ej = static_cast<int>(idx / static_cast<unsigned long long>(p.nx));
+        et = tc;
+    } else if (e5) {
+        const unsigned long long idx = ~e5;
+        status = SWE_ERR_INSTABILITY; kind = 5;
+        ei = static_cast<int>(idx % static_cast<unsigned long long>(p.nx));
+        ej = static_cast<int>(idx / static_cast<unsigned long long>(p.nx));
+        et = tc;
+    } else if (dg || p.always_diag || !(msx < p.tz_x) || !(msy < p.tz_y)) {
+        status = SWE_STATUS_DIAG;
+    } else {
+        const double a = __ddiv_rn(p.dx, msx);
+        const double b = __ddiv_rn(p.dy, msy);
+        const double core = (b < a) ? b : a;
+        const double dt_raw = std_min(p.cfl * core, p.dt_max);
+        dt_next = dt_raw;
+        if (dt_raw < p.dt_min) {
+            status = SWE_ERR_STEP_COLLAPSE; kind = 6; edt = dt_raw; et = tc;
+        }
+    }
+    c->max_sx = msx;
+    c->max_sy = msy;
+    c->dt_used = dt;
+    c->t_commit = tc;
+    c->dt_next = dt_next;
+    c->status = status;
+    c->err_kind = kind;
+    c->err_i = ei;
+    c->err_j = ej;
+    c->err_t = et;
+    c->err_dt = edt;
+    if (status == 0) {
+        c->sel ^= 1;
+        c->t = tc;
+        c->step_index += 1ull;
+        c->dt_raw = dt_next;
+        c->steps_done += 1ull;
+        c->done = (c->mode == 1) ? !(tc < c->t_end) : 0;
+    } else {
+        c->done = 1;
+    }
+    for (int k = 0; k < RED_N; ++k) red[k] = 0ull;
+    c->finish = 0u;
+    c->work = 0u;
+    __threadfence();
+}
+
+// --------------------------------------------------------------- the kernel
+// One warp = one worker.  Lane t owns column i = x0 - R + t of a 32-column
+// window; lanes R..31-R are output columns.  Iteration k of the row march is
+// a 3-stage software pipeline over consecutive rows (march direction S):
+//   stage 1  row b+S : committed row from the warp's TMA ring; F/G/S(U)
+//   stage 2  row b   : predictor U*, F/G/S(U*), interface fluxes, boundary
+//                      faces, dry-U* detection
+//   stage 3  row b-S : corrector (+ smoothing of row b-2S), guard, CFL, store
+// The three dependency chains interleave within the warp; x neighbours are
+// exchanged with shuffles, so warps never wait for each other.  The steady
+// state is unrolled by two with the pipeline registers ping-ponging between
+// two carry sets, so no register moves are needed to advance the march.
+
+// Pipeline registers entering an iteration.
 struct Carry {
-    Flux FU[2];
-    double srx[2], sry[2];   // S(U) of row b (Manning only)
-    CellVec Hyp[2];          // y face (b-S, b)
-    CellVec Cp[2], Cpp[2];   // corrector rows b-S, b-2S (smoothing)
+    CellVec U;                 // committed state of the stage-2 row b
+    Flux FU;                   // its fluxes
+    double srx, sry, zx, zy;   // its source term and bed slopes
+    CellVec Hyp;               // y face (b-S, b)
+    CellVec Uc;                // committed state of the stage-3 row c = b-S
+    double c_srx, c_sry, c_ssx, c_ssy;  // S(U) and S(U*) of row c
+    CellVec c_hs, c_hn, c_hx;  // y faces and own x face of row c
+    CellVec Cp, Cpp;           // corrector output of rows c-S, c-2S (smoothing)
+};
+
+struct WarpRing {  // per-warp TMA ring state (warp-uniform)
+    int d;         // stage of the next request to consume
+    unsigned ph;   // its mbarrier phase parity
 };
 
 template <int WPB, bool FWD, bool SMOOTH, bool FLAT, bool MANNING, bool EXACT>
@@ -32,46 +220,48 @@ struct Marcher {
     static constexpr int S = FWD ? 1 : -1;
     static constexpr int NF = FLAT ? 3 : 5;
     static constexpr int D = kStages;
-    static constexpr int W = 64;           // window columns
-    static constexpr int XH = SWE_XOFF;    // halo columns per side (2: keeps TMA boxes 16-byte aligned)
-    static constexpr int TW = W - 2 * XH;  // output columns per window
-    static constexpr int QN = 4;
+    static constexpr int TW = 32 - 2 * R;
     static constexpr unsigned FULL = 0xffffffffu;
 
-    static constexpr int NO = 3;  // output staging buffers (TMA store ring)
-    static constexpr int OB = (3 * TW + 15) / 16 * 16;  // doubles per staging buffer (128-byte aligned)
     const StepParams& p;
     double* stage;
-    double* ostage;  // [NO][3][TW] staged output rows
-    int obuf;        // next output staging buffer
     unsigned long long* bars;
-    Seg* segq;
-    int qhead, qtail;
+    Seg* segq;      // per-warp queue of claimed work items (ring of QN)
+    int qhead, qtail;  // consumer / producer positions (warp-uniform)
     int lane;
+    const double* cur;
     double* nxt;
     int P;
-    double dt, dtdx, dtdy, half_dt, h_min, half_g, neg_g, gnn, cx, cy;
+    double dt, dtdx, dtdy, half_dt, h_min, half_g, neg_g, gnn;
+    // producer state (lanes < NF): next request
     int pleft;
     bool pdone;
-    int px, py, pzy, sel;
+    const double* psrc;
+    const double* pzsrc;
+    int px, py, sel;  // TMA tensor coordinates of the next request; committed buffer
+    long long pstep;
     int pn, req;
     WarpRing ring;
-    int dprev;           // ring slot of the previously consumed row (row b during iteration k)
-    int i0, L, r_start;  // i0: global column of the lane's first cell
-    int tile_x;
-    bool in_x[2], out_x[2], star_ok[2], xedge;
+    // per-segment constants
+    int i, L, r_start;
+    bool in_x, out_x, star_ok, xedge;
+    // reductions
     double mx, my;
-    unsigned long long e4, e5;
-    int e2;
+    unsigned long long e2, e4, e5;
 
-    static __device__ __forceinline__ double face(double a, double b) {
-        if constexpr (EXACT) return 0.5 * (a + b);
-        else return a + b;
+    __device__ __forceinline__ double shf_nb(double x) const {
+        return FWD ? __shfl_down_sync(FULL, x, 1) : __shfl_up_sync(FULL, x, 1);
     }
-    // value of the neighbouring lane towards +x (down) / -x (up)
-    static __device__ __forceinline__ double from_right(double x) { return __shfl_down_sync(FULL, x, 1); }
-    static __device__ __forceinline__ double from_left(double x) { return __shfl_up_sync(FULL, x, 1); }
+    __device__ __forceinline__ double shf_back(double x) const {
+        return FWD ? __shfl_up_sync(FULL, x, 1) : __shfl_down_sync(FULL, x, 1);
+    }
+    static __device__ __forceinline__ double avg(double a, double b) { return 0.5 * (a + b); }
 
+    static constexpr int QN = 4;
+    // Producer: claim the next work item (tile, row chunk) from the step's
+    // atomic counter, queue it for the consumer and point this lane at its
+    // first row.  Dynamic claiming balances the cheaper interior windows
+    // against the boundary windows and any per-SM speed differences.
     __device__ __forceinline__ void prod_seg() {
         unsigned item = 0;
         if (lane == 0) item = atomicAdd(&p.ctl->work, 1u);
@@ -82,8 +272,8 @@ struct Marcher {
             pdone = true;
             return;
         }
-        const int rc = static_cast<int>(item / p.ntiles);
-        const int tile = static_cast<int>(item % p.ntiles);
+        const int rc = static_cast<int>(item / p.ntiles);   // row-chunk major: neighbouring
+        const int tile = static_cast<int>(item % p.ntiles); // windows share halo sectors in L2
         Seg sg;
         sg.tile = tile;
         sg.ra = rc * p.chunk;
@@ -92,465 +282,401 @@ struct Marcher {
         ++qtail;
         pleft = (sg.rb - sg.ra) + 2 * R;
         const int row = FWD ? sg.ra - R : sg.rb - 1 + R;
-        px = tile * TW;  // padded column of the window start
-        py = (row + R) * 3;
-        pzy = (row + R) * 2;
+        const size_t col0 = static_cast<size_t>(sg.tile) * TW;  // padded offset of x0-R
+        if constexpr (SWE_LOADER == 2) {
+            px = static_cast<int>(col0);
+            py = (row + R) * 3;
+        } else if constexpr (SWE_LOADER == 0) {
+            if (lane < 3) {
+                psrc = cur + (static_cast<size_t>(row + R) * 3 + lane) * P + col0;
+                pstep = static_cast<long long>(S) * 3 * P;
+            } else {
+                psrc = p.slope + (static_cast<size_t>(row + R) * 2 + (lane - 3)) * P + col0;
+                pstep = static_cast<long long>(S) * 2 * P;
+            }
+        } else {
+            psrc = cur + static_cast<size_t>(row + R) * 3 * P + col0 + lane;
+            pstep = static_cast<long long>(S) * 3 * P;
+            if constexpr (!FLAT) pzsrc = p.slope + static_cast<size_t>(row + R) * 2 * P + col0 + lane;
+        }
     }
     __device__ __forceinline__ void produce() {
-#ifdef SWE_COMPUTEONLY
-        if (pleft == 0 && !(pdone || qtail - qhead >= QN - 1)) prod_seg();
-        if (pleft > 0) {
-            --pleft;
-            ++pn;
-        }
-        return;
-#endif
-        while (pn < req + D - 2) {  // keep the slots of rows b and b+S resident
+        while (pn < req + D - 1) {
             if (pleft == 0 && !(pdone || qtail - qhead >= QN - 1)) prod_seg();
-            if (pleft == 0) return;
-            const int d = pn % D;
-            if (lane == 0) {
-                mbar_expect_tx(&bars[d], NF * W * 8);
-                tma_load_2d(stage + d * NF * W, &p.tmap_state[sel], px, py, &bars[d]);
-                if constexpr (!FLAT) tma_load_2d(stage + d * NF * W + 3 * W, &p.tmap_slope, px, pzy, &bars[d]);
-                if constexpr (SWE_PF > 0) {  // warm L2 for the row SWE_PF requests later (same window)
-                    if (pleft > SWE_PF) {
-                        tma_prefetch_2d(&p.tmap_state[sel], px, py + S * 3 * SWE_PF);
-                        if constexpr (!FLAT) tma_prefetch_2d(&p.tmap_slope, px, pzy + S * 2 * SWE_PF);
-                    }
+            if (pleft == 0) {
+                if constexpr (SWE_LOADER == 1) {  // keep one commit group per request slot
+                    cp_async_commit();
+                    ++pn;
+                    continue;
                 }
+                return;
             }
-            py += S * 3;
-            pzy += S * 2;
+            const int d = pn % D;
+            if constexpr (SWE_LOADER == 2) {
+                if (lane == 0) {
+                    mbar_expect_tx(&bars[d], NF * 32 * 8);
+                    tma_load_2d(stage + d * NF * 32, &p.tmap_state[sel], px, py, &bars[d]);
+                    if constexpr (!FLAT) tma_load_2d(stage + d * NF * 32 + 96, &p.tmap_slope, px, (py / 3) * 2, &bars[d]);
+                }
+                py += S * 3;
+            } else if constexpr (SWE_LOADER == 0) {
+                if (lane == 0) mbar_expect_tx(&bars[d], NF * 32 * 8);
+                __syncwarp();
+                if (lane < NF) bulk_g2s(stage + (d * NF + lane) * 32, psrc, 32 * 8, &bars[d]);
+            } else {
+                double* dst = stage + d * NF * 32 + lane;
+                cp_async8(dst, psrc);
+                cp_async8(dst + 32, psrc + P);
+                cp_async8(dst + 64, psrc + 2 * P);
+                if constexpr (!FLAT) {
+                    cp_async8(dst + 96, pzsrc);
+                    cp_async8(dst + 128, pzsrc + P);
+                    pzsrc += static_cast<long long>(S) * 2 * P;
+                }
+                cp_async_commit();
+            }
+            if constexpr (SWE_LOADER != 2) psrc += pstep;
             --pleft;
             ++pn;
         }
     }
-    // read the two cells of a resident ring slot
-    __device__ __forceinline__ void read_slot(int d, CellVec (&u)[2], double (&zx)[2], double (&zy)[2]) const {
-#ifdef SWE_COMPUTEONLY
-        {
-            const double r = 1e-6 * static_cast<double>(d);
-            u[0] = {1.0 + r + 1e-5 * lane, 0.01 + r, 0.002 - r};
-            u[1] = {1.0 - r + 2e-5 * lane, 0.012 - r, 0.001 + r};
-            zx[0] = zx[1] = FLAT ? 0.0 : 1e-5;
-            zy[0] = zy[1] = 0.0;
-            return;
-        }
-#endif
-        const double* st = stage + d * NF * W + 2 * lane;
-        const double2 h = *reinterpret_cast<const double2*>(st);
-        const double2 qx = *reinterpret_cast<const double2*>(st + W);
-        const double2 qy = *reinterpret_cast<const double2*>(st + 2 * W);
-        u[0] = {h.x, qx.x, qy.x};
-        u[1] = {h.y, qx.y, qy.y};
+    __device__ __forceinline__ void consume(CellVec& u, double& zx, double& zy) {
+        if constexpr (SWE_LOADER != 1) mbar_wait(&bars[ring.d], ring.ph);
+        else cp_async_wait<D - 2>();  // groups are committed one per request slot
+        const double* st = stage + ring.d * NF * 32;
+        u.h = st[lane];
+        u.qx = st[32 + lane];
+        u.qy = st[64 + lane];
         if constexpr (!FLAT) {
-            const double2 a = *reinterpret_cast<const double2*>(st + 3 * W);
-            const double2 c = *reinterpret_cast<const double2*>(st + 4 * W);
-            zx[0] = a.x;
-            zx[1] = a.y;
-            zy[0] = c.x;
-            zy[1] = c.y;
+            zx = st[96 + lane];
+            zy = st[128 + lane];
         } else {
-            zx[0] = zx[1] = zy[0] = zy[1] = 0.0;
-        }
-    }
-    __device__ __forceinline__ void consume(CellVec (&u)[2], double (&zx)[2], double (&zy)[2]) {
-#ifdef SWE_COMPUTEONLY
-        {
-            const double r = 1e-6 * static_cast<double>(req & 15);
-            u[0] = {1.0 + r + 1e-5 * lane, 0.01 + r, 0.002 - r};
-            u[1] = {1.0 - r + 2e-5 * lane, 0.012 - r, 0.001 + r};
-            zx[0] = zx[1] = FLAT ? 0.0 : 1e-5;
-            zy[0] = zy[1] = 0.0;
-            dprev = ring.d;
-            if (++ring.d == D) {
-                ring.d = 0;
-                ring.ph ^= 1u;
-            }
-            ++req;
-            return;
-        }
-#endif
-        mbar_wait(&bars[ring.d], ring.ph);
-        dprev = ring.d;
-        const double* st = stage + ring.d * NF * W + 2 * lane;
-        const double2 h = *reinterpret_cast<const double2*>(st);
-        const double2 qx = *reinterpret_cast<const double2*>(st + W);
-        const double2 qy = *reinterpret_cast<const double2*>(st + 2 * W);
-        u[0] = {h.x, qx.x, qy.x};
-        u[1] = {h.y, qx.y, qy.y};
-        if constexpr (!FLAT) {
-            const double2 a = *reinterpret_cast<const double2*>(st + 3 * W);
-            const double2 c = *reinterpret_cast<const double2*>(st + 4 * W);
-            zx[0] = a.x;
-            zx[1] = a.y;
-            zy[0] = c.x;
-            zy[1] = c.y;
-        } else {
-            zx[0] = zx[1] = zy[0] = zy[1] = 0.0;
+            zx = 0.0;
+            zy = 0.0;
         }
         if (++ring.d == D) {
             ring.d = 0;
             ring.ph ^= 1u;
         }
         ++req;
-    }
-    __device__ __forceinline__ void fluxes(const CellVec& u, double zx, double zy, Flux& f, double& sx,
-                                           double& sy) const {
-        const Rc rc = A::recip(u.h);
-        f = A::flux(u, rc, half_g);
-        source_of<EXACT, MANNING>(u, f, rc, zx, zy, neg_g, gnn, sx, sy);
+        __syncwarp();
+        produce();
     }
 
-    // guard + CFL + store of the lane's two cells of row rr (executor.hpp:543-580)
-    __device__ __forceinline__ void emit2(const CellVec (&o)[2], int rr) {
-        bool bad[2];
-        double* row = nxt + static_cast<size_t>(rr + R) * 3 * P + (i0 + XH);
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            const bool ok = finite_d(o[c].h) && finite_d(o[c].qx) && finite_d(o[c].qy) && o[c].h >= h_min;
-            const Rc rc = A::recip(o[c].h);
-            const double cc = A::sqrt_(p.g * o[c].h);
-            double u, v;
-            A::div2(o[c].qx, o[c].qy, rc, u, v);
-            const double sx = fabs(u) + cc, sy = fabs(v) + cc;
-            if (out_x[c]) {
-                mx = fmax(mx, sx);
-                my = fmax(my, sy);
-            }
-            bad[c] = out_x[c] && !ok;
-        }
-#if defined(SWE_COMPUTEONLY) && !defined(SWE_KEEPSTORES) || defined(SWE_NOSTORES)
-        if (o[0].h == -12345.0) row[0] = o[1].qx + o[0].qy;  // never true: keeps the values live
-        if (true) return;
-#endif
-        if (!xedge) {  // stage the row and hand it to the TMA engine (asynchronous)
-            bulk_wait_read<NO - 1>();  // the buffer reused now has been read by its store
-            __syncwarp();
-            double* ob = ostage + obuf * OB;
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                const int t = 2 * lane + c - XH;  // output column within the window
-                if (out_x[c]) {
-                    ob[t] = o[c].h;
-                    ob[TW + t] = o[c].qx;
-                    ob[2 * TW + t] = o[c].qy;
-                }
-            }
-            fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-                tma_store_2d(&p.tmap_out[sel ^ 1], tile_x, (rr + R) * 3, ob);
-                bulk_commit();
-            }
-            if (++obuf == NO) obuf = 0;
-        } else if (out_x[0] && out_x[1]) {  // 16-byte stores (the column pair is 16-byte aligned)
-            *reinterpret_cast<double2*>(row) = make_double2(o[0].h, o[1].h);
-            *reinterpret_cast<double2*>(row + P) = make_double2(o[0].qx, o[1].qx);
-            *reinterpret_cast<double2*>(row + 2 * P) = make_double2(o[0].qy, o[1].qy);
-        } else {
-#pragma unroll
-            for (int c = 0; c < 2; ++c)
-                if (out_x[c]) {
-                    row[c] = o[c].h;
-                    row[P + c] = o[c].qx;
-                    row[2 * P + c] = o[c].qy;
-                }
-        }
+    // output cell: guard (K5), CFL (K6), store, ghosts for the next step (K1)
+    __device__ __forceinline__ void emit(const CellVec& o, int rr) {
         const int jj = p.j0 + rr;
-        if (__any_sync(FULL, bad[0] || bad[1])) {
-            for (int c = 1; c >= 0; --c)
-                if (bad[c]) e5 = max(e5, ~(static_cast<unsigned long long>(jj) * p.nx + (i0 + c)));
+        const bool ok = finite_d(o.h) && finite_d(o.qx) && finite_d(o.qy) && o.h >= h_min;
+        if (!ok) e5 = max(e5, ~(static_cast<unsigned long long>(jj) * p.nx + i));
+        const Rc rc = A::recip(o.h);  // executor.hpp:560-580
+        const double c = A::sqrt_(p.g * o.h);
+        double u, v;
+        A::div2(o.qx, o.qy, rc, u, v);
+        mx = fmax(mx, fabs(u) + c);
+        my = fmax(my, fabs(v) + c);
+        double* row = nxt + static_cast<size_t>(rr + R) * 3 * P + (i + R);
+        row[0] = o.h;
+        row[P] = o.qx;
+        row[2 * P] = o.qy;
+        if (!(xedge || jj == 0 || jj == p.ny - 1)) return;
+        if (i == 0) {
+            const CellVec g = edge_ghost(SWE_EDGE_W, p.bc[SWE_EDGE_W], o, p.z_w[rr + R], h_min);
+            row[-1] = g.h;
+            row[P - 1] = g.qx;
+            row[2 * P - 1] = g.qy;
         }
-        if (xedge || jj == 0 || jj == p.ny - 1) {
-            for (int c = 0; c < 2; ++c) {
-                const int ic = i0 + c;
-                if (out_x[c] && (ic == 0 || ic == p.nx - 1 || jj == 0 || jj == p.ny - 1))
-                    write_ghosts(row + c, P, o[c], ic, jj, p.nx, p.ny, p.bc, p.z_w[rr + R], p.z_e[rr + R],
-                                 p.z_s[ic], p.z_n[ic], h_min);
+        if (i == p.nx - 1) {
+            const CellVec g = edge_ghost(SWE_EDGE_E, p.bc[SWE_EDGE_E], o, p.z_e[rr + R], h_min);
+            row[1] = g.h;
+            row[P + 1] = g.qx;
+            row[2 * P + 1] = g.qy;
+        }
+        if (jj == 0) {
+            const CellVec g = edge_ghost(SWE_EDGE_S, p.bc[SWE_EDGE_S], o, p.z_s[i], h_min);
+            double* gr = row - 3 * P;
+            gr[0] = g.h;
+            gr[P] = g.qx;
+            gr[2 * P] = g.qy;
+        }
+        if (jj == p.ny - 1) {
+            const CellVec g = edge_ghost(SWE_EDGE_N, p.bc[SWE_EDGE_N], o, p.z_n[i], h_min);
+            double* gr = row + 3 * P;
+            gr[0] = g.h;
+            gr[P] = g.qx;
+            gr[2 * P] = g.qy;
+        }
+    }
+
+    // boundary faces of row b (executor.hpp:471-514): walls carry pressure only,
+    // inflow the flux of the pump states, the other kinds use U* ghosts.
+    // Updates the own x face Hx and the y faces; returns the x face that belongs
+    // to the neighbouring out-of-domain lane (handed over by the caller).
+    __device__ __forceinline__ void boundary_faces(int b, int jb, const CellVec& U, const Flux& FU, const CellVec& Us,
+                                                const Flux& FS, CellVec& Hx, CellVec& hy_a, CellVec& hy_b,
+                                                CellVec& xo, int& give) {
+        give = 0;
+        if (!(i >= 0 && i < p.nx && jb >= 0 && jb < p.ny)) return;
+        const unsigned long long idx = static_cast<unsigned long long>(jb) * p.nx + i;
+        if (i == 0) {
+            const SweBC& bc = p.bc[SWE_EDGE_W];
+            CellVec w = Hx;
+            bool set = true;
+            if (bc.type == SWE_BC_WALL) {
+                w = {0.0, avg(FU.fxx, FS.fxx), 0.0};
+            } else if (bc.type == SWE_BC_INFLOW) {
+                const CellVec a = flux_x_plain(pump_state(SWE_EDGE_W, bc.q_n, U), half_g);
+                const CellVec c = flux_x_plain(pump_state(SWE_EDGE_W, bc.q_n, Us), half_g);
+                w = {avg(a.h, c.h), avg(a.qx, c.qx), avg(a.qy, c.qy)};
+            } else if (FWD) {
+                const CellVec g = edge_ghost(SWE_EDGE_W, bc, Us, p.z_w[b + R], h_min);
+                if (!(g.h >= h_min)) e4 = max(e4, ~idx);
+                const CellVec c = flux_x_plain(g, half_g);
+                w = {avg(U.qx, c.h), avg(FU.fxx, c.qx), avg(FU.fxy, c.qy)};
+            } else {
+                set = false;
+            }
+            if (set) {
+                if (FWD) { xo = w; give = 1; }  // the west face is lane t-1's
+                else Hx = w;
+            }
+        }
+        if (i == p.nx - 1) {
+            const SweBC& bc = p.bc[SWE_EDGE_E];
+            CellVec e = Hx;
+            bool set = true;
+            if (bc.type == SWE_BC_WALL) {
+                e = {0.0, avg(FU.fxx, FS.fxx), 0.0};
+            } else if (bc.type == SWE_BC_INFLOW) {
+                const CellVec a = flux_x_plain(pump_state(SWE_EDGE_E, bc.q_n, U), half_g);
+                const CellVec c = flux_x_plain(pump_state(SWE_EDGE_E, bc.q_n, Us), half_g);
+                e = {avg(a.h, c.h), avg(a.qx, c.qx), avg(a.qy, c.qy)};
+            } else if (!FWD) {
+                const CellVec g = edge_ghost(SWE_EDGE_E, bc, Us, p.z_e[b + R], h_min);
+                if (!(g.h >= h_min)) e4 = max(e4, ~idx);
+                const CellVec c = flux_x_plain(g, half_g);
+                e = {avg(U.qx, c.h), avg(FU.fxx, c.qx), avg(FU.fxy, c.qy)};
+            } else {
+                set = false;
+            }
+            if (set) {
+                if (FWD) Hx = e;
+                else { xo = e; give = 1; }  // the east face is lane t+1's
+            }
+        }
+        if (jb == 0) {
+            const SweBC& bc = p.bc[SWE_EDGE_S];
+            CellVec f = {0.0, 0.0, 0.0};
+            bool set = true;
+            if (bc.type == SWE_BC_WALL) {
+                f = {0.0, 0.0, avg(FU.gyy, FS.gyy)};
+            } else if (bc.type == SWE_BC_INFLOW) {
+                const CellVec a = flux_y_plain(pump_state(SWE_EDGE_S, bc.q_n, U), half_g);
+                const CellVec c = flux_y_plain(pump_state(SWE_EDGE_S, bc.q_n, Us), half_g);
+                f = {avg(a.h, c.h), avg(a.qx, c.qx), avg(a.qy, c.qy)};
+            } else if (FWD) {
+                const CellVec g = edge_ghost(SWE_EDGE_S, bc, Us, p.z_s[i], h_min);
+                if (!(g.h >= h_min)) e4 = max(e4, ~idx);
+                const CellVec c = flux_y_plain(g, half_g);
+                f = {avg(U.qy, c.h), avg(FU.fxy, c.qx), avg(FU.gyy, c.qy)};
+            } else {
+                set = false;
+            }
+            if (set) {
+                if (FWD) hy_a = f;
+                else hy_b = f;
+            }
+        }
+        if (jb == p.ny - 1) {
+            const SweBC& bc = p.bc[SWE_EDGE_N];
+            CellVec f = {0.0, 0.0, 0.0};
+            bool set = true;
+            if (bc.type == SWE_BC_WALL) {
+                f = {0.0, 0.0, avg(FU.gyy, FS.gyy)};
+            } else if (bc.type == SWE_BC_INFLOW) {
+                const CellVec a = flux_y_plain(pump_state(SWE_EDGE_N, bc.q_n, U), half_g);
+                const CellVec c = flux_y_plain(pump_state(SWE_EDGE_N, bc.q_n, Us), half_g);
+                f = {avg(a.h, c.h), avg(a.qx, c.qx), avg(a.qy, c.qy)};
+            } else if (!FWD) {
+                const CellVec g = edge_ghost(SWE_EDGE_N, bc, Us, p.z_n[i], h_min);
+                if (!(g.h >= h_min)) e4 = max(e4, ~idx);
+                const CellVec c = flux_y_plain(g, half_g);
+                f = {avg(U.qy, c.h), avg(FU.fxy, c.qx), avg(FU.gyy, c.qy)};
+            } else {
+                set = false;
+            }
+            if (set) {
+                if (FWD) hy_b = f;
+                else hy_a = f;
             }
         }
     }
 
-    template <bool DO3, bool EMIT>
+    // One iteration k of the march: `in` -> `out`.
+    template <bool DO12, bool DO3, bool EMIT>
     __device__ __forceinline__ void iter(int k, const Carry& in, Carry& out) {
-        const int b = r_start + S * k;
-        const int jb = p.j0 + b;
-        const int dslot_b = dprev;  // row b's ring slot
-        CellVec Un[2];
-        double zxn[2], zyn[2];
-        consume(Un, zxn, zyn);
-        // row b, re-read from its resident slot
-        CellVec Ub[2];
-        double zxb[2], zyb[2];
-        read_slot(dslot_b, Ub, zxb, zyb);
-        // ---- stage 1: fluxes (and Manning source) of row b+S
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            const Rc rc = A::recip(Un[c].h);
-            out.FU[c] = A::flux(Un[c], rc, half_g);
-            if constexpr (MANNING)
-                source_of<EXACT, MANNING>(Un[c], out.FU[c], rc, zxn[c], zyn[c], neg_g, gnn, out.srx[c], out.sry[c]);
-        }
-        // source of row b: carried (Manning) or recomputed (scheme.hpp:54-63, fr = 0)
-        double srxb[2], sryb[2];
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            if constexpr (MANNING) {
-                srxb[c] = in.srx[c];
-                sryb[c] = in.sry[c];
-            } else {
-                const double gh = neg_g * Ub[c].h;
-                srxb[c] = gh * zxb[c] - 0.0 * Ub[c].qx;
-                sryb[c] = gh * zyb[c] - 0.0 * Ub[c].qy;
-            }
-        }
-        // ---- stage 2: predictor of row b   scheme.hpp:100-113
-        // F of the x neighbour each cell differences with
-        double fn_h[2], fn_qx[2], fn_qy[2];
-        if constexpr (FWD) {
-            fn_h[0] = Ub[1].qx;
-            fn_qx[0] = in.FU[1].fxx;
-            fn_qy[0] = in.FU[1].fxy;
-            fn_h[1] = from_right(Ub[0].qx);
-            fn_qx[1] = from_right(in.FU[0].fxx);
-            fn_qy[1] = from_right(in.FU[0].fxy);
-        } else {
-            fn_h[1] = Ub[0].qx;
-            fn_qx[1] = in.FU[0].fxx;
-            fn_qy[1] = in.FU[0].fxy;
-            fn_h[0] = from_left(Ub[1].qx);
-            fn_qx[0] = from_left(in.FU[1].fxx);
-            fn_qy[0] = from_left(in.FU[1].fxy);
-        }
-        CellVec Us[2], Hx[2], hs[2], hn[2];
-        Flux FS[2];
-        double ssx[2], ssy[2];
-        bool dry[2];
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            const CellVec& U = Ub[c];
-            const Flux& FU = in.FU[c];
-            const Flux& FN = out.FU[c];
+        const int b = r_start + S * k;  // stage-2 row (local)
+        if constexpr (DO12) {
+            // ======== stage 1: committed row b+S
+            consume(out.U, out.zx, out.zy);
+            const Rc rcN = A::recip(out.U.h);
+            out.FU = A::flux(out.U, rcN, half_g);
+            source_of<EXACT, MANNING>(out.U, out.FU, rcN, out.zx, out.zy, neg_g, gnn, out.srx, out.sry);
+
+            // ======== stage 2: predictor at (i, b)   scheme.hpp:100-113
+            const CellVec& U = in.U;
+            const Flux& FU = in.FU;
+            const CellVec& Un = out.U;
+            const Flux& FN = out.FU;
+            const double fn_h = shf_nb(U.qx);
+            const double fn_qx = shf_nb(FU.fxx);
+            const double fn_qy = shf_nb(FU.fxy);
             double df_h, df_qx, df_qy, dg_h, dg_qx, dg_qy;
             if constexpr (FWD) {
-                df_h = fn_h[c] - U.qx; df_qx = fn_qx[c] - FU.fxx; df_qy = fn_qy[c] - FU.fxy;
-                dg_h = Un[c].qy - U.qy; dg_qx = FN.fxy - FU.fxy; dg_qy = FN.gyy - FU.gyy;
+                df_h = fn_h - U.qx; df_qx = fn_qx - FU.fxx; df_qy = fn_qy - FU.fxy;
+                dg_h = Un.qy - U.qy; dg_qx = FN.fxy - FU.fxy; dg_qy = FN.gyy - FU.gyy;
             } else {
-                df_h = U.qx - fn_h[c]; df_qx = FU.fxx - fn_qx[c]; df_qy = FU.fxy - fn_qy[c];
-                dg_h = U.qy - Un[c].qy; dg_qx = FU.fxy - FN.fxy; dg_qy = FU.gyy - FN.gyy;
+                df_h = U.qx - fn_h; df_qx = FU.fxx - fn_qx; df_qy = FU.fxy - fn_qy;
+                dg_h = U.qy - Un.qy; dg_qx = FU.fxy - FN.fxy; dg_qy = FU.gyy - FN.gyy;
             }
-            if constexpr (EXACT) {
-                Us[c].h = (U.h - (dtdx * df_h + dtdy * dg_h)) + 0.0;
-                Us[c].qx = (U.qx - (dtdx * df_qx + dtdy * dg_qx)) + dt * srxb[c];
-                Us[c].qy = (U.qy - (dtdx * df_qy + dtdy * dg_qy)) + dt * sryb[c];
-            } else {
-                Us[c].h = U.h - __fma_rn(dtdx, df_h, dtdy * dg_h);
-                Us[c].qx = __fma_rn(dt, srxb[c], U.qx - __fma_rn(dtdx, df_qx, dtdy * dg_qx));
-                Us[c].qy = __fma_rn(dt, sryb[c], U.qy - __fma_rn(dtdx, df_qy, dtdy * dg_qy));
+            CellVec Us;
+            Us.h = (U.h - (dtdx * df_h + dtdy * dg_h)) + 0.0;
+            Us.qx = (U.qx - (dtdx * df_qx + dtdy * dg_qx)) + dt * in.srx;
+            Us.qy = (U.qy - (dtdx * df_qy + dtdy * dg_qy)) + dt * in.sry;
+
+            const int jb = p.j0 + b;
+            // dry U* -> row-major first consumer (executor.hpp:429-436, 459-513)
+            if (!(Us.h >= h_min) && star_ok && in_x && jb >= 0 && jb < p.ny) {
+                unsigned long long cons;
+                if (FWD) cons = static_cast<unsigned long long>(jb) * p.nx + i;
+                else if (jb >= 1) cons = static_cast<unsigned long long>(jb - 1) * p.nx + i;
+                else if (i >= 1) cons = static_cast<unsigned long long>(jb) * p.nx + (i - 1);
+                else cons = static_cast<unsigned long long>(jb) * p.nx + i;
+                e4 = max(e4, ~cons);
             }
-            dry[c] = !(Us[c].h >= h_min) && star_ok[c] && in_x[c];
-            if (!(U.h >= h_min) && k >= 0 && k < L && out_x[c]) e2 = 1;
-            fluxes(Us[c], zxb[c], zyb[c], FS[c], ssx[c], ssy[c]);
-            Hx[c] = {face(fn_h[c], Us[c].qx), face(fn_qx[c], FS[c].fxx), face(fn_qy[c], FS[c].fxy)};
-            out.Hyp[c] = {face(Un[c].qy, Us[c].qy), face(FN.fxy, FS[c].fxy), face(FN.gyy, FS[c].gyy)};
-            hs[c] = FWD ? in.Hyp[c] : out.Hyp[c];
-            hn[c] = FWD ? out.Hyp[c] : in.Hyp[c];
-        }
-        if (__any_sync(FULL, dry[0] || dry[1])) {  // dry U* -> first consumer (executor.hpp:459-513)
-            for (int c = 0; c < 2; ++c) {
-                const int ic = i0 + c;
-                if (dry[c] && jb >= 0 && jb < p.ny) {
-                    unsigned long long cons;
-                    if (FWD) cons = static_cast<unsigned long long>(jb) * p.nx + ic;
-                    else if (jb >= 1) cons = static_cast<unsigned long long>(jb - 1) * p.nx + ic;
-                    else if (ic >= 1) cons = static_cast<unsigned long long>(jb) * p.nx + (ic - 1);
-                    else cons = static_cast<unsigned long long>(jb) * p.nx + ic;
-                    e4 = max(e4, ~cons);
+            // K2 precondition on the committed state (scheme.hpp:35-39)
+            if (!(U.h >= h_min) && k >= 0 && k < L && out_x) e2 = 1;
+
+            const Rc rcS = A::recip(Us.h);
+            const Flux FS = A::flux(Us, rcS, half_g);
+            source_of<EXACT, MANNING>(Us, FS, rcS, in.zx, in.zy, neg_g, gnn, out.c_ssx, out.c_ssy);
+
+            // own x face (FWD: east, BWD: west) and y face (b, b+S)   scheme.hpp:153-161
+            CellVec Hx = {avg(fn_h, Us.qx), avg(fn_qx, FS.fxx), avg(fn_qy, FS.fxy)};
+            out.Hyp = {avg(Un.qy, Us.qy), avg(FN.fxy, FS.fxy), avg(FN.gyy, FS.gyy)};
+            CellVec hy_a = in.Hyp, hy_b = out.Hyp;  // faces (b-S, b) and (b, b+S)
+            if (xedge || jb == 0 || jb == p.ny - 1) {  // warp-uniform
+                CellVec xo = {0.0, 0.0, 0.0};
+                int give = 0;
+                boundary_faces(b, jb, U, FU, Us, FS, Hx, hy_a, hy_b, xo, give);
+                if (xedge) {  // hand the boundary face to the out-of-domain lane that owns it
+                    const double gh = shf_nb(xo.h), gqx = shf_nb(xo.qx), gqy = shf_nb(xo.qy);
+                    const int gv = FWD ? __shfl_down_sync(FULL, give, 1) : __shfl_up_sync(FULL, give, 1);
+                    if (gv && i == (FWD ? -1 : p.nx)) Hx = {gh, gqx, gqy};
                 }
             }
+            out.c_hs = FWD ? hy_a : hy_b;
+            out.c_hn = FWD ? hy_b : hy_a;
+            out.c_hx = Hx;
+            out.Uc = U;
+            out.c_srx = in.srx;
+            out.c_sry = in.sry;
         }
-        // boundary faces (edge windows / rows only); FWD hands the west face of i=0
-        // to the cell at i=-1, BWD the east face of i=nx-1 to the cell at i=nx
-        if (xedge || jb == 0 || jb == p.ny - 1) {
-            CellVec give_f[2] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
-            int give[2] = {0, 0};
-            for (int c = 0; c < 2; ++c) {
-                const int ic = i0 + c;
-                if (in_x[c] && jb >= 0 && jb < p.ny && (ic == 0 || ic == p.nx - 1 || jb == 0 || jb == p.ny - 1)) {
-                    EdgeIn ei;
-                    ei.U = Ub[c];
-                    ei.Us = Us[c];
-                    ei.fu_xx = in.FU[c].fxx;
-                    ei.fu_xy = in.FU[c].fxy;
-                    ei.fu_yy = in.FU[c].gyy;
-                    ei.fs_xx = FS[c].fxx;
-                    ei.fs_xy = FS[c].fxy;
-                    ei.fs_yy = FS[c].gyy;
-                    ei.Hx = Hx[c];
-                    ei.hy_a = FWD ? hs[c] : hn[c];
-                    ei.hy_b = FWD ? hn[c] : hs[c];
-                    const EdgeOut eo = boundary_faces<FWD>(ei, ic, jb, p.nx, p.ny, p.bc, p.z_w[b + R], p.z_e[b + R],
-                                                           p.z_s[ic], p.z_n[ic], h_min, half_g, e4, !EXACT);
-                    Hx[c] = eo.Hx;
-                    hs[c] = FWD ? eo.hy_a : eo.hy_b;
-                    hn[c] = FWD ? eo.hy_b : eo.hy_a;
-                    e4 = eo.e4;
-                    give[c] = eo.give;
-                    give_f[c] = eo.xo;
-                }
-            }
-            if (xedge) {
-                if constexpr (FWD) {  // face of cell c goes to cell c-1 (lane-1's cell 1 for c = 0)
-                    if (give[1]) Hx[0] = give_f[1];
-                    const double gh = from_right(give_f[0].h), gqx = from_right(give_f[0].qx),
-                                 gqy = from_right(give_f[0].qy);
-                    const int gv = __shfl_down_sync(FULL, give[0], 1);
-                    if (gv) Hx[1] = {gh, gqx, gqy};
-                } else {              // face of cell c goes to cell c+1 (lane+1's cell 0 for c = 1)
-                    if (give[0]) Hx[1] = give_f[0];
-                    const double gh = from_left(give_f[1].h), gqx = from_left(give_f[1].qx),
-                                 gqy = from_left(give_f[1].qy);
-                    const int gv = __shfl_up_sync(FULL, give[1], 1);
-                    if (gv) Hx[0] = {gh, gqx, gqy};
-                }
-            }
-        }
-        // ---- stage 3: corrector of row b   scheme.hpp:185-191
+
         if constexpr (DO3) {
-            CellVec hw[2], he[2];
-            if constexpr (FWD) {  // own face is the east face
-                he[0] = Hx[0];
-                he[1] = Hx[1];
-                hw[1] = Hx[0];
-                hw[0] = {from_left(Hx[1].h), from_left(Hx[1].qx), from_left(Hx[1].qy)};
-            } else {              // own face is the west face
-                hw[0] = Hx[0];
-                hw[1] = Hx[1];
-                he[0] = Hx[1];
-                he[1] = {from_right(Hx[0].h), from_right(Hx[0].qx), from_right(Hx[0].qy)};
-            }
-            CellVec C[2];
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                const CellVec& U = Ub[c];
-                const double sx_ = srxb[c] + ssx[c], sy_ = sryb[c] + ssy[c];
-                if constexpr (EXACT) {
-                    const double fs_h = dtdx * (he[c].h - hw[c].h) + dtdy * (hn[c].h - hs[c].h);
-                    const double fs_qx = dtdx * (he[c].qx - hw[c].qx) + dtdy * (hn[c].qx - hs[c].qx);
-                    const double fs_qy = dtdx * (he[c].qy - hw[c].qy) + dtdy * (hn[c].qy - hs[c].qy);
-                    C[c].h = (U.h - fs_h) + 0.0;
-                    C[c].qx = (U.qx - fs_qx) + half_dt * sx_;
-                    C[c].qy = (U.qy - fs_qy) + half_dt * sy_;
-                } else {
-                    const double fs_h = __fma_rn(cx, he[c].h - hw[c].h, cy * (hn[c].h - hs[c].h));
-                    const double fs_qx = __fma_rn(cx, he[c].qx - hw[c].qx, cy * (hn[c].qx - hs[c].qx));
-                    const double fs_qy = __fma_rn(cx, he[c].qy - hw[c].qy, cy * (hn[c].qy - hs[c].qy));
-                    C[c].h = U.h - fs_h;
-                    C[c].qx = __fma_rn(half_dt, sx_, U.qx - fs_qx);
-                    C[c].qy = __fma_rn(half_dt, sy_, U.qy - fs_qy);
-                }
-            }
+            // ======== stage 3: corrector of row c = b - S   scheme.hpp:185-191
+            const CellVec ot = {shf_back(in.c_hx.h), shf_back(in.c_hx.qx), shf_back(in.c_hx.qy)};
+            const CellVec hw = FWD ? ot : in.c_hx, he = FWD ? in.c_hx : ot;
+            const double fs_h = dtdx * (he.h - hw.h) + dtdy * (in.c_hn.h - in.c_hs.h);
+            const double fs_qx = dtdx * (he.qx - hw.qx) + dtdy * (in.c_hn.qx - in.c_hs.qx);
+            const double fs_qy = dtdx * (he.qy - hw.qy) + dtdy * (in.c_hn.qy - in.c_hs.qy);
+            CellVec C;
+            C.h = (in.Uc.h - fs_h) + 0.0;
+            C.qx = (in.Uc.qx - fs_qx) + half_dt * (in.c_srx + in.c_ssx);
+            C.qy = (in.Uc.qy - fs_qy) + half_dt * (in.c_sry + in.c_ssy);
+            const int c_row = b - S;
             if constexpr (!SMOOTH) {
-                if constexpr (EMIT) emit2(C, b);
+                if (EMIT && out_x) emit(C, c_row);
             } else {
-                if constexpr (EMIT) {  // smoothing of row q = b - S (executor.hpp:533-540)
-                    const CellVec* Cp = in.Cp;
-                    CellVec ce[2], cw[2];
-                    ce[0] = Cp[1];
-                    cw[1] = Cp[0];
-                    ce[1] = {from_right(Cp[0].h), from_right(Cp[0].qx), from_right(Cp[0].qy)};
-                    cw[0] = {from_left(Cp[1].h), from_left(Cp[1].qx), from_left(Cp[1].qy)};
-                    const int q = b - S;
-                    const int jq = p.j0 + q;
-                    CellVec o[2];
-#pragma unroll
-                    for (int c = 0; c < 2; ++c) {
-                        CellVec cn = FWD ? C[c] : in.Cpp[c];
-                        CellVec cs = FWD ? in.Cpp[c] : C[c];
-                        CellVec e = ce[c], w = cw[c];
+                // smoothing of row q = c - S   (executor.hpp:533-540, scheme.hpp:197-204)
+                const CellVec& Cp = in.Cp;
+                if constexpr (EMIT) {
+                    CellVec ce = {__shfl_down_sync(FULL, Cp.h, 1), __shfl_down_sync(FULL, Cp.qx, 1),
+                                  __shfl_down_sync(FULL, Cp.qy, 1)};
+                    CellVec cw = {__shfl_up_sync(FULL, Cp.h, 1), __shfl_up_sync(FULL, Cp.qx, 1),
+                                  __shfl_up_sync(FULL, Cp.qy, 1)};
+                    if (out_x) {
+                        const int q = c_row - S;
+                        const int jq = p.j0 + q;
+                        CellVec cn = FWD ? C : in.Cpp;
+                        CellVec cs = FWD ? in.Cpp : C;
                         if (xedge || jq == 0 || jq == p.ny - 1) {
-                            const int ic = i0 + c;
-                            if (ic == 0) w = edge_ghost(SWE_EDGE_W, p.bc[SWE_EDGE_W], Cp[c], p.z_w[q + R], h_min);
-                            if (ic == p.nx - 1)
-                                e = edge_ghost(SWE_EDGE_E, p.bc[SWE_EDGE_E], Cp[c], p.z_e[q + R], h_min);
-                            if (jq == 0) cs = edge_ghost(SWE_EDGE_S, p.bc[SWE_EDGE_S], Cp[c], p.z_s[ic], h_min);
-                            if (jq == p.ny - 1)
-                                cn = edge_ghost(SWE_EDGE_N, p.bc[SWE_EDGE_N], Cp[c], p.z_n[ic], h_min);
+                            if (i == 0) cw = edge_ghost(SWE_EDGE_W, p.bc[SWE_EDGE_W], Cp, p.z_w[q + R], h_min);
+                            if (i == p.nx - 1) ce = edge_ghost(SWE_EDGE_E, p.bc[SWE_EDGE_E], Cp, p.z_e[q + R], h_min);
+                            if (jq == 0) cs = edge_ghost(SWE_EDGE_S, p.bc[SWE_EDGE_S], Cp, p.z_s[i], h_min);
+                            if (jq == p.ny - 1) cn = edge_ghost(SWE_EDGE_N, p.bc[SWE_EDGE_N], Cp, p.z_n[i], h_min);
                         }
                         const double nu = p.nu;
-                        const CellVec& u = Cp[c];
-                        o[c].h = u.h + nu * (((e.h - u.h) + (w.h - u.h)) + ((cn.h - u.h) + (cs.h - u.h)));
-                        o[c].qx = u.qx + nu * (((e.qx - u.qx) + (w.qx - u.qx)) + ((cn.qx - u.qx) + (cs.qx - u.qx)));
-                        o[c].qy = u.qy + nu * (((e.qy - u.qy) + (w.qy - u.qy)) + ((cn.qy - u.qy) + (cs.qy - u.qy)));
+                        CellVec o;
+                        o.h = Cp.h + nu * (((ce.h - Cp.h) + (cw.h - Cp.h)) + ((cn.h - Cp.h) + (cs.h - Cp.h)));
+                        o.qx = Cp.qx + nu * (((ce.qx - Cp.qx) + (cw.qx - Cp.qx)) + ((cn.qx - Cp.qx) + (cs.qx - Cp.qx)));
+                        o.qy = Cp.qy + nu * (((ce.qy - Cp.qy) + (cw.qy - Cp.qy)) + ((cn.qy - Cp.qy) + (cs.qy - Cp.qy)));
+                        emit(o, q);
                     }
-                    emit2(o, q);
                 }
-#pragma unroll
-                for (int c = 0; c < 2; ++c) {
-                    out.Cpp[c] = in.Cp[c];
-                    out.Cp[c] = C[c];
-                }
+                out.Cpp = Cp;
+                out.Cp = C;
             }
         }
-        produce();
     }
 
+    // March one segment: output rows [ra, rb) of one 32-column window.
     __device__ __forceinline__ void segment(const Seg& sg) {
         L = sg.rb - sg.ra;
-        const int xw0 = sg.tile * TW - XH;  // global column of lane 0's first cell
-        tile_x = sg.tile * TW + XH;         // padded column of the first output column
-        i0 = xw0 + 2 * lane;
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            const int ic = i0 + c;
-            const int t = 2 * lane + c;  // column within the window
-            in_x[c] = (ic >= 0) && (ic < p.nx);
-            out_x[c] = in_x[c] && t >= XH && t < W - XH;
-            star_ok[c] = FWD ? (t < W - 1) : (t > 0);
-        }
-        xedge = (xw0 <= 0) || (xw0 + W - 1 >= p.nx - 1);
+        const int xw0 = sg.tile * TW - R;  // global column of lane 0
+        i = xw0 + lane;
+        in_x = (i >= 0) && (i < p.nx);
+        out_x = in_x && lane >= R && lane < 32 - R;
+        star_ok = FWD ? (lane < 31) : (lane > 0);
+        xedge = (xw0 <= 0) || (xw0 + 31 >= p.nx - 1);
         r_start = FWD ? sg.ra : sg.rb - 1;
+
         Carry A, B;
+        // pre-iteration: committed row r_start - S*R
+        consume(A.U, A.zx, A.zy);
         {
-            CellVec u[2];
-            double zx[2], zy[2];
-            consume(u, zx, zy);
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                const Rc rc = A::recip(u[c].h);
-                A.FU[c] = A::flux(u[c], rc, half_g);
-                A.srx[c] = A.sry[c] = 0.0;
-                if constexpr (MANNING)
-                    source_of<EXACT, MANNING>(u[c], A.FU[c], rc, zx[c], zy[c], neg_g, gnn, A.srx[c], A.sry[c]);
-            }
+            const Rc rc = A::recip(A.U.h);
+            A.FU = A::flux(A.U, rc, half_g);
+            source_of<EXACT, MANNING>(A.U, A.FU, rc, A.zx, A.zy, neg_g, gnn, A.srx, A.sry);
         }
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            A.Hyp[c] = {0.0, 0.0, 0.0};
-            A.Cp[c] = {0.0, 0.0, 0.0};
-            A.Cpp[c] = {0.0, 0.0, 0.0};
-        }
-        produce();
-        int k = -R;
-        if constexpr (SMOOTH) {
-            iter<false, false>(k++, A, B);  // row -2: predictor only
-            A = B;
-            iter<true, false>(k++, A, B);   // rows -1, 0: correctors feeding the first smoothed row
-            A = B;
-            iter<true, false>(k++, A, B);
-            A = B;
+        A.Hyp = {0.0, 0.0, 0.0};
+        A.Cp = {0.0, 0.0, 0.0};
+        A.Cpp = {0.0, 0.0, 0.0};
+        int k;
+        if constexpr (!SMOOTH) {
+            // k = -1, 0: no corrector yet; 1..L-1 steady; L: corrector only
+            iter<true, false, false>(-1, A, B);
+            iter<true, false, false>(0, B, A);
+            k = 1;
         } else {
-            iter<false, false>(k++, A, B);  // row -1: predictor only
-            A = B;
+            // k = -2, -1: no corrector; 0, 1: corrector without output;
+            // 2..L steady; L+1: corrector + smoothing only
+            iter<true, false, false>(-2, A, B);
+            iter<true, false, false>(-1, B, A);
+            iter<true, true, false>(0, A, B);
+            iter<true, true, false>(1, B, A);
+            k = 2;
         }
-        const int k_last = SMOOTH ? L : L - 1;
+        const int k_last = SMOOTH ? L : L - 1;  // last steady iteration
         for (; k + 1 <= k_last; k += 2) {
-            iter<true, true>(k, A, B);
-            iter<true, true>(k + 1, B, A);
+            iter<true, true, true>(k, A, B);
+            iter<true, true, true>(k + 1, B, A);
         }
-        if (k <= k_last) iter<true, true>(k, A, B);
+        if (k <= k_last) {  // odd steady count
+            iter<true, true, true>(k, A, B);
+            iter<false, true, true>(k + 1, B, A);
+        } else {
+            iter<false, true, true>(k, A, B);
+        }
     }
 };
 
@@ -559,7 +685,6 @@ __global__ void __launch_bounds__(WPB * 32, SWE_MINB) swe_step_kernel(const __gr
     using M = Marcher<WPB, FWD, SMOOTH, FLAT, MANNING, EXACT>;
     constexpr int D = kStages;
     constexpr int NF = M::NF;
-    constexpr int W = M::W;
     constexpr unsigned FULL = 0xffffffffu;
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -572,12 +697,9 @@ __global__ void __launch_bounds__(WPB * 32, SWE_MINB) swe_step_kernel(const __gr
     __shared__ double s_dt, s_tc;
     __shared__ double s_red[2][WPB];
     SweCtl* ctl = p.ctl;
-    double* stage = reinterpret_cast<double*>(smem_raw) + warp * (D * NF * W);  // [D][NF][64]
-    double* ostage = reinterpret_cast<double*>(smem_raw) + WPB * D * NF * W + warp * (M::NO * M::OB);
+    double* stage = reinterpret_cast<double*>(smem_raw) + warp * (D * NF * 32);  // [D][NF][32]
     unsigned long long* bars =
-        reinterpret_cast<unsigned long long*>(reinterpret_cast<double*>(smem_raw) + WPB * D * NF * W +
-                                              WPB * M::NO * M::OB) +
-        warp * D;
+        reinterpret_cast<unsigned long long*>(reinterpret_cast<double*>(smem_raw) + WPB * D * NF * 32) + warp * D;
 
     if (tid == 0) {
         const volatile SweCtl* vc = ctl;
@@ -610,45 +732,44 @@ __global__ void __launch_bounds__(WPB * 32, SWE_MINB) swe_step_kernel(const __gr
 
     M m{p};
     m.stage = stage;
-    m.ostage = ostage;
-    m.obuf = 0;
     m.bars = bars;
     m.segq = segq_all[warp];
     m.qhead = 0;
     m.qtail = 0;
     m.lane = lane;
+    m.cur = p.buf[s_sel];
     m.sel = s_sel;
+    m.px = 0;
+    m.py = 0;
     m.nxt = p.buf[s_sel ^ 1];
     m.P = p.pitch;
     m.dt = s_dt;
-    m.dtdx = m.dt / p.dx;
+    m.dtdx = m.dt / p.dx;  // scheme.hpp:110, 188-190
     m.dtdy = m.dt / p.dy;
     m.half_dt = 0.5 * m.dt;
-    m.cx = EXACT ? m.dtdx : 0.5 * m.dtdx;
-    m.cy = EXACT ? m.dtdy : 0.5 * m.dtdy;
     m.h_min = p.h_min;
     m.half_g = p.half_g;
     m.neg_g = p.neg_g;
     m.gnn = p.gnn;
     m.pleft = 0;
     m.pdone = false;
-    m.px = m.py = m.pzy = 0;
+    m.pzsrc = nullptr;
+    m.psrc = nullptr;
+    m.pstep = 0;
     m.pn = 0;
     m.req = 0;
     m.ring = {0, 0u};
-    m.dprev = 0;
     m.mx = 0.0;
     m.my = 0.0;
-    m.e2 = 0;
-    m.e4 = m.e5 = 0ull;
+    m.e2 = m.e4 = m.e5 = 0ull;
     m.produce();
-    while (m.qhead < m.qtail) {
+    while (m.qhead < m.qtail) {  // the producer keeps the queue ahead of the consumer
         const Seg sg = m.segq[m.qhead % M::QN];
         ++m.qhead;
         m.segment(sg);
     }
 
-    bulk_wait_all();  // this warp's TMA row stores are complete
+    // ---- CTA reduction of the CFL maxima and error words
     double mx = m.mx, my = m.my;
     for (int o = 16; o > 0; o >>= 1) {
         mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
@@ -687,8 +808,7 @@ __global__ void __launch_bounds__(WPB * 32, SWE_MINB) swe_step_kernel(const __gr
 
 template <int WPB, bool SMOOTH, bool FLAT>
 constexpr size_t step_smem_bytes() {
-    return static_cast<size_t>(WPB) * kStages * (FLAT ? 3 : 5) * 64 * 8 +
-           WPB * 3 * ((3 * (64 - 2 * SWE_XOFF) + 15) / 16 * 16) * 8 + WPB * kStages * 8;
+    return static_cast<size_t>(WPB) * kStages * (FLAT ? 3 : 5) * 32 * 8 + WPB * kStages * 8;
 }
 
 }  // namespace swe_dev

@@ -20,13 +20,10 @@ namespace {
 constexpr int kWPB = SWE_STEP_WPB;  // warps (independent workers) per CTA
 constexpr bool kExact = SWE_EXACT_TU != 0;
 
-#define SWE_KERNEL_T swe_dev::swe_step_kernel
-#define SWE_SMEM_T swe_dev::step_smem_bytes
-
 template <bool FWD, bool SMOOTH, bool FLAT, bool MANNING>
 cudaError_t launch_one(int grid, cudaStream_t s, const StepParams& p) {
-    constexpr size_t smem = SWE_SMEM_T<kWPB, SMOOTH, FLAT>();
-    auto k = SWE_KERNEL_T<kWPB, FWD, SMOOTH, FLAT, MANNING, kExact>;
+    constexpr size_t smem = swe_dev::step_smem_bytes<kWPB, SMOOTH, FLAT>();
+    auto k = swe_dev::swe_step_kernel<kWPB, FWD, SMOOTH, FLAT, MANNING, kExact>;
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -40,8 +37,8 @@ cudaError_t launch_one(int grid, cudaStream_t s, const StepParams& p) {
 
 template <bool FWD, bool SMOOTH, bool FLAT, bool MANNING>
 int occupancy_one() {
-    constexpr size_t smem = SWE_SMEM_T<kWPB, SMOOTH, FLAT>();
-    auto k = SWE_KERNEL_T<kWPB, FWD, SMOOTH, FLAT, MANNING, kExact>;
+    constexpr size_t smem = swe_dev::step_smem_bytes<kWPB, SMOOTH, FLAT>();
+    auto k = swe_dev::swe_step_kernel<kWPB, FWD, SMOOTH, FLAT, MANNING, kExact>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     int n = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kWPB * 32, smem) != cudaSuccess) return 1;

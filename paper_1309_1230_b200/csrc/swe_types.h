@@ -10,11 +10,6 @@
 
 enum { SWE_EDGE_N = 0, SWE_EDGE_S = 1, SWE_EDGE_E = 2, SWE_EDGE_W = 3 };
 
-// Padded x layout: global column i lives at padded column i + SWE_XOFF; the
-// ghost column of the west edge is padded column SWE_XOFF - 1.  Two columns
-// keep every TMA box (load window start, store row start) 16-byte aligned.
-#define SWE_XOFF 2
-
 struct SweBC {
     int type;  // swe_bc_type
     double q_n;
@@ -68,7 +63,6 @@ struct StepParams {
     // (box 32 x 3 = h, qx, qy of one row); slopes as [2*(nloc+2R)][P] (box 32 x 2)
     CUtensorMap tmap_state[2];
     CUtensorMap tmap_slope;
-    CUtensorMap tmap_out[2];  // state buffer k, box (output columns per window) x 3: TMA row stores
     double* buf[2];        // committed/candidate state, row-interleaved SoA
     const double* slope;   // dzdx/dzdy rows, same layout; nullptr for a flat bed
     const double* z_w;     // bed z at i=0 per local row
