@@ -232,7 +232,7 @@ struct Marcher {
     const double* cur;
     double* nxt;
     int P;
-    double dt, dtdx, dtdy, half_dt, h_min, half_g, neg_g, gnn;
+    double dt, dtdx, dtdy, half_dt, h_min, half_g, neg_g, gnn, cx, cy;
     // producer state (lanes < NF): next request
     int pleft;
     bool pdone;
@@ -255,7 +255,12 @@ struct Marcher {
     __device__ __forceinline__ double shf_back(double x) const {
         return FWD ? __shfl_up_sync(FULL, x, 1) : __shfl_down_sync(FULL, x, 1);
     }
-    static __device__ __forceinline__ double avg(double a, double b) { return 0.5 * (a + b); }
+    // Interface flux 0.5*(F(U) + F(U*)) (scheme.hpp:153-161).  FAST mode keeps
+    // the plain sum and folds the 0.5 into the corrector coefficients cx/cy.
+    static __device__ __forceinline__ double avg(double a, double b) {
+        if constexpr (EXACT) return 0.5 * (a + b);
+        else return a + b;
+    }
 
     static constexpr int QN = 4;
     // Producer: claim the next work item (tile, row chunk) from the step's
@@ -366,14 +371,21 @@ struct Marcher {
     // output cell: guard (K5), CFL (K6), store, ghosts for the next step (K1)
     __device__ __forceinline__ void emit(const CellVec& o, int rr) {
         const int jj = p.j0 + rr;
-        const bool ok = finite_d(o.h) && finite_d(o.qx) && finite_d(o.qy) && o.h >= h_min;
-        if (!ok) e5 = max(e5, ~(static_cast<unsigned long long>(jj) * p.nx + i));
         const Rc rc = A::recip(o.h);  // executor.hpp:560-580
         const double c = A::sqrt_(p.g * o.h);
         double u, v;
         A::div2(o.qx, o.qy, rc, u, v);
-        mx = fmax(mx, fabs(u) + c);
-        my = fmax(my, fabs(v) + c);
+        const double sx = fabs(u) + c, sy = fabs(v) + c;
+        // guard (executor.hpp:543-558): a non-finite h, qx or qy always makes
+        // sx + sy non-finite, so one test screens the cell; the exact test
+        // runs only for the rare cell that fails the screen.
+        if (!(finite_d(sx + sy) && o.h >= h_min)) {
+            const bool ok = finite_d(o.h) && finite_d(o.qx) && finite_d(o.qy) && o.h >= h_min;
+            if (!ok) e5 = max(e5, ~(static_cast<unsigned long long>(jj) * p.nx + i));
+        }
+        // CFL maxima; a NaN speed (only in a guarded cell) never replaces them
+        mx = (sx > mx) ? sx : mx;
+        my = (sy > my) ? sy : my;
         double* row = nxt + static_cast<size_t>(rr + R) * 3 * P + (i + R);
         row[0] = o.h;
         row[P] = o.qx;
@@ -539,9 +551,15 @@ struct Marcher {
                 dg_h = U.qy - Un.qy; dg_qx = FU.fxy - FN.fxy; dg_qy = FU.gyy - FN.gyy;
             }
             CellVec Us;
-            Us.h = (U.h - (dtdx * df_h + dtdy * dg_h)) + 0.0;
-            Us.qx = (U.qx - (dtdx * df_qx + dtdy * dg_qx)) + dt * in.srx;
-            Us.qy = (U.qy - (dtdx * df_qy + dtdy * dg_qy)) + dt * in.sry;
+            if constexpr (EXACT) {
+                Us.h = (U.h - (dtdx * df_h + dtdy * dg_h)) + 0.0;
+                Us.qx = (U.qx - (dtdx * df_qx + dtdy * dg_qx)) + dt * in.srx;
+                Us.qy = (U.qy - (dtdx * df_qy + dtdy * dg_qy)) + dt * in.sry;
+            } else {
+                Us.h = U.h - __fma_rn(dtdx, df_h, dtdy * dg_h);
+                Us.qx = __fma_rn(dt, in.srx, U.qx - __fma_rn(dtdx, df_qx, dtdy * dg_qx));
+                Us.qy = __fma_rn(dt, in.sry, U.qy - __fma_rn(dtdx, df_qy, dtdy * dg_qy));
+            }
 
             const int jb = p.j0 + b;
             // dry U* -> row-major first consumer (executor.hpp:429-436, 459-513)
@@ -586,13 +604,22 @@ struct Marcher {
             // ======== stage 3: corrector of row c = b - S   scheme.hpp:185-191
             const CellVec ot = {shf_back(in.c_hx.h), shf_back(in.c_hx.qx), shf_back(in.c_hx.qy)};
             const CellVec hw = FWD ? ot : in.c_hx, he = FWD ? in.c_hx : ot;
-            const double fs_h = dtdx * (he.h - hw.h) + dtdy * (in.c_hn.h - in.c_hs.h);
-            const double fs_qx = dtdx * (he.qx - hw.qx) + dtdy * (in.c_hn.qx - in.c_hs.qx);
-            const double fs_qy = dtdx * (he.qy - hw.qy) + dtdy * (in.c_hn.qy - in.c_hs.qy);
             CellVec C;
-            C.h = (in.Uc.h - fs_h) + 0.0;
-            C.qx = (in.Uc.qx - fs_qx) + half_dt * (in.c_srx + in.c_ssx);
-            C.qy = (in.Uc.qy - fs_qy) + half_dt * (in.c_sry + in.c_ssy);
+            if constexpr (EXACT) {
+                const double fs_h = dtdx * (he.h - hw.h) + dtdy * (in.c_hn.h - in.c_hs.h);
+                const double fs_qx = dtdx * (he.qx - hw.qx) + dtdy * (in.c_hn.qx - in.c_hs.qx);
+                const double fs_qy = dtdx * (he.qy - hw.qy) + dtdy * (in.c_hn.qy - in.c_hs.qy);
+                C.h = (in.Uc.h - fs_h) + 0.0;
+                C.qx = (in.Uc.qx - fs_qx) + half_dt * (in.c_srx + in.c_ssx);
+                C.qy = (in.Uc.qy - fs_qy) + half_dt * (in.c_sry + in.c_ssy);
+            } else {  // faces are plain sums here: cx = dt/(2dx), cy = dt/(2dy)
+                const double fs_h = __fma_rn(cx, he.h - hw.h, cy * (in.c_hn.h - in.c_hs.h));
+                const double fs_qx = __fma_rn(cx, he.qx - hw.qx, cy * (in.c_hn.qx - in.c_hs.qx));
+                const double fs_qy = __fma_rn(cx, he.qy - hw.qy, cy * (in.c_hn.qy - in.c_hs.qy));
+                C.h = in.Uc.h - fs_h;
+                C.qx = __fma_rn(half_dt, in.c_srx + in.c_ssx, in.Uc.qx - fs_qx);
+                C.qy = __fma_rn(half_dt, in.c_sry + in.c_ssy, in.Uc.qy - fs_qy);
+            }
             const int c_row = b - S;
             if constexpr (!SMOOTH) {
                 if (EMIT && out_x) emit(C, c_row);
@@ -747,6 +774,8 @@ __global__ void __launch_bounds__(WPB * 32, SWE_MINB) swe_step_kernel(const __gr
     m.dtdx = m.dt / p.dx;  // scheme.hpp:110, 188-190
     m.dtdy = m.dt / p.dy;
     m.half_dt = 0.5 * m.dt;
+    m.cx = EXACT ? m.dtdx : 0.5 * m.dtdx;
+    m.cy = EXACT ? m.dtdy : 0.5 * m.dtdy;
     m.h_min = p.h_min;
     m.half_g = p.half_g;
     m.neg_g = p.neg_g;
