@@ -712,7 +712,7 @@ EXPORT int swe_cuda_create(const swe_grid* grid, const swe_physics* phys, const 
     {
         std::string err;
         for (int k = 0; k < 2; ++k)
-            if (!encode_rows(&p.tmap_state[k], c->d_buf[k], c->pitch, static_cast<long long>(rows) * 3, 3, err))
+            if (!encode_rows(&p.tmap_state[k], c->d_buf[k], c->pitch, static_cast<long long>(rows) * 3, 3 * SWE_ROW_GROUP, err))
                 return set_status(st, SWE_ERR_RUNTIME, -1, -1, 0, "%s", err.c_str());
     }
     p.buf[0] = c->d_buf[0];
@@ -845,7 +845,7 @@ EXPORT int swe_cuda_load(swe_ctx* c, const double* z, const double* h, const dou
     c->prm.slope = c->d_slope;
     {
         std::string err;
-        if (!encode_rows(&c->prm.tmap_slope, c->d_slope, P, static_cast<long long>(nloc + 2 * R) * 2, 2, err))
+        if (!encode_rows(&c->prm.tmap_slope, c->d_slope, P, static_cast<long long>(nloc + 2 * R) * 2, 2 * SWE_ROW_GROUP, err))
             return set_status(st, SWE_ERR_RUNTIME, -1, -1, 0, "%s", err.c_str());
     }
 

@@ -10,6 +10,7 @@
 #define SWE_STEP_WPB 4   // warps per CTA; every warp is an independent row-march worker
 #endif
 #define SWE_TILE_W(R) (32 - 2 * (R))  // output columns per warp window
+#define SWE_ROW_GROUP 2               // rows per TMA request (state box 32 x 3G, slope box 32 x 2G)
 
 inline int swe_step_variant(bool fwd, bool smooth, bool flat, bool manning) {
     return (fwd ? 8 : 0) | (smooth ? 4 : 0) | (flat ? 2 : 0) | (manning ? 1 : 0);

@@ -29,10 +29,11 @@
 #pragma once
 
 #include "swe_device.cuh"
+#include "swe_launch.h"
 
 namespace swe_dev {
 
-constexpr int kStages = 5;
+constexpr int kStages = 4;  // ring depth in row groups (8 rows in flight)
 #ifndef SWE_MINB
 #define SWE_MINB 3
 #endif
@@ -82,18 +83,10 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-#ifndef SWE_LOADER
-#define SWE_LOADER 2  // 0: 1D bulk copies; 1: per-lane cp.async (LDGSTS); 2: 2D TMA tensor maps
-#endif
+// Rows per TMA request: one 2D box carries G consecutive rows (state box
+// 32 x 3G, slope box 32 x 2G), so the per-request issue cost (uniform-register
+// setup, mbarrier arm/wait, ring bookkeeping) is paid once per G rows.
+constexpr int kGroup = SWE_ROW_GROUP;
 
 // ------------------------------------------------------------ work partition
 // Worker w (one warp) owns units [w*U/G, (w+1)*U/G) of the unit space
@@ -220,6 +213,8 @@ struct Marcher {
     static constexpr int S = FWD ? 1 : -1;
     static constexpr int NF = FLAT ? 3 : 5;
     static constexpr int D = kStages;
+    static constexpr int G = kGroup;
+    static constexpr int SLOT = NF * G * 32;  // doubles per ring slot: [G][3][32] state, [G][2][32] slopes
     static constexpr int TW = 32 - 2 * R;
     static constexpr unsigned FULL = 0xffffffffu;
 
@@ -233,14 +228,12 @@ struct Marcher {
     double* nxt;
     int P;
     double dt, dtdx, dtdy, half_dt, h_min, half_g, neg_g, gnn, cx, cy;
-    // producer state (lanes < NF): next request
+    // producer state (warp-uniform): row groups left in the current segment,
+    // TMA coordinates of the next request, committed buffer
     int pleft;
     bool pdone;
-    const double* psrc;
-    const double* pzsrc;
-    int px, py, sel;  // TMA tensor coordinates of the next request; committed buffer
-    long long pstep;
-    int pn, req;
+    int px, py, sel;
+    int pn, req;  // row groups requested / fully consumed
     WarpRing ring;
     // per-segment constants
     int i, L, r_start;
@@ -285,80 +278,46 @@ struct Marcher {
         sg.rb = min(sg.ra + p.chunk, p.nloc);
         segq[qtail % QN] = sg;
         ++qtail;
-        pleft = (sg.rb - sg.ra) + 2 * R;
-        const int row = FWD ? sg.ra - R : sg.rb - 1 + R;
-        const size_t col0 = static_cast<size_t>(sg.tile) * TW;  // padded offset of x0-R
-        if constexpr (SWE_LOADER == 2) {
-            px = static_cast<int>(col0);
-            py = (row + R) * 3;
-        } else if constexpr (SWE_LOADER == 0) {
-            if (lane < 3) {
-                psrc = cur + (static_cast<size_t>(row + R) * 3 + lane) * P + col0;
-                pstep = static_cast<long long>(S) * 3 * P;
-            } else {
-                psrc = p.slope + (static_cast<size_t>(row + R) * 2 + (lane - 3)) * P + col0;
-                pstep = static_cast<long long>(S) * 2 * P;
-            }
-        } else {
-            psrc = cur + static_cast<size_t>(row + R) * 3 * P + col0 + lane;
-            pstep = static_cast<long long>(S) * 3 * P;
-            if constexpr (!FLAT) pzsrc = p.slope + static_cast<size_t>(row + R) * 2 * P + col0 + lane;
-        }
+        pleft = ((sg.rb - sg.ra) + 2 * R + G - 1) / G;
+        const int row = FWD ? sg.ra - R : sg.rb - 1 + R;  // first row in march order
+        px = sg.tile * TW;                                // padded column of x0-R
+        py = (FWD ? row : row - (G - 1)) + R;             // lowest padded row of the first group
     }
     __device__ __forceinline__ void produce() {
         while (pn < req + D - 1) {
             if (pleft == 0 && !(pdone || qtail - qhead >= QN - 1)) prod_seg();
-            if (pleft == 0) {
-                if constexpr (SWE_LOADER == 1) {  // keep one commit group per request slot
-                    cp_async_commit();
-                    ++pn;
-                    continue;
-                }
-                return;
-            }
+            if (pleft == 0) return;
             const int d = pn % D;
-            if constexpr (SWE_LOADER == 2) {
-                if (lane == 0) {
-                    mbar_expect_tx(&bars[d], NF * 32 * 8);
-                    tma_load_2d(stage + d * NF * 32, &p.tmap_state[sel], px, py, &bars[d]);
-                    if constexpr (!FLAT) tma_load_2d(stage + d * NF * 32 + 96, &p.tmap_slope, px, (py / 3) * 2, &bars[d]);
-                }
-                py += S * 3;
-            } else if constexpr (SWE_LOADER == 0) {
-                if (lane == 0) mbar_expect_tx(&bars[d], NF * 32 * 8);
-                __syncwarp();
-                if (lane < NF) bulk_g2s(stage + (d * NF + lane) * 32, psrc, 32 * 8, &bars[d]);
-            } else {
-                double* dst = stage + d * NF * 32 + lane;
-                cp_async8(dst, psrc);
-                cp_async8(dst + 32, psrc + P);
-                cp_async8(dst + 64, psrc + 2 * P);
-                if constexpr (!FLAT) {
-                    cp_async8(dst + 96, pzsrc);
-                    cp_async8(dst + 128, pzsrc + P);
-                    pzsrc += static_cast<long long>(S) * 2 * P;
-                }
-                cp_async_commit();
+            if (lane == 0) {
+                mbar_expect_tx(&bars[d], SLOT * 8);
+                tma_load_2d(stage + d * SLOT, &p.tmap_state[sel], px, py * 3, &bars[d]);
+                if constexpr (!FLAT) tma_load_2d(stage + d * SLOT + 3 * G * 32, &p.tmap_slope, px, py * 2, &bars[d]);
             }
-            if constexpr (SWE_LOADER != 2) psrc += pstep;
+            py += S * G;
             --pleft;
             ++pn;
         }
     }
+    // Row GI (in march order) of the current group.  Groups never span two
+    // segments; the march's row count is static modulo G = 2 (see segment()).
+    template <int GI>
     __device__ __forceinline__ void consume(CellVec& u, double& zx, double& zy) {
-        if constexpr (SWE_LOADER != 1) mbar_wait(&bars[ring.d], ring.ph);
-        else cp_async_wait<D - 2>();  // groups are committed one per request slot
-        const double* st = stage + ring.d * NF * 32;
-        u.h = st[lane];
-        u.qx = st[32 + lane];
-        u.qy = st[64 + lane];
+        if constexpr (GI == 0) mbar_wait(&bars[ring.d], ring.ph);
+        constexpr int g = FWD ? GI : G - 1 - GI;  // row within the box (boxes ascend in y)
+        const double* st = stage + ring.d * SLOT;
+        u.h = st[g * 96 + lane];
+        u.qx = st[g * 96 + 32 + lane];
+        u.qy = st[g * 96 + 64 + lane];
         if constexpr (!FLAT) {
-            zx = st[96 + lane];
-            zy = st[128 + lane];
+            zx = st[G * 96 + g * 64 + lane];
+            zy = st[G * 96 + g * 64 + 32 + lane];
         } else {
             zx = 0.0;
             zy = 0.0;
         }
+        if constexpr (GI == G - 1) next_group();
+    }
+    __device__ __forceinline__ void next_group() {
         if (++ring.d == D) {
             ring.d = 0;
             ring.ph ^= 1u;
@@ -524,12 +483,12 @@ struct Marcher {
     }
 
     // One iteration k of the march: `in` -> `out`.
-    template <bool DO12, bool DO3, bool EMIT>
+    template <bool DO12, bool DO3, bool EMIT, int GI = 0>
     __device__ __forceinline__ void iter(int k, const Carry& in, Carry& out) {
         const int b = r_start + S * k;  // stage-2 row (local)
         if constexpr (DO12) {
             // ======== stage 1: committed row b+S
-            consume(out.U, out.zx, out.zy);
+            consume<GI>(out.U, out.zx, out.zy);
             const Rc rcN = A::recip(out.U.h);
             out.FU = A::flux(out.U, rcN, half_g);
             source_of<EXACT, MANNING>(out.U, out.FU, rcN, out.zx, out.zy, neg_g, gnn, out.srx, out.sry);
@@ -669,7 +628,7 @@ struct Marcher {
 
         Carry A, B;
         // pre-iteration: committed row r_start - S*R
-        consume(A.U, A.zx, A.zy);
+        consume<0>(A.U, A.zx, A.zy);  // march row 0
         {
             const Rc rc = A::recip(A.U.h);
             A.FU = A::flux(A.U, rc, half_g);
@@ -681,27 +640,30 @@ struct Marcher {
         int k;
         if constexpr (!SMOOTH) {
             // k = -1, 0: no corrector yet; 1..L-1 steady; L: corrector only
-            iter<true, false, false>(-1, A, B);
-            iter<true, false, false>(0, B, A);
+            iter<true, false, false, 1>(-1, A, B);
+            iter<true, false, false, 0>(0, B, A);
             k = 1;
         } else {
             // k = -2, -1: no corrector; 0, 1: corrector without output;
             // 2..L steady; L+1: corrector + smoothing only
-            iter<true, false, false>(-2, A, B);
-            iter<true, false, false>(-1, B, A);
-            iter<true, true, false>(0, A, B);
-            iter<true, true, false>(1, B, A);
+            iter<true, false, false, 1>(-2, A, B);
+            iter<true, false, false, 0>(-1, B, A);
+            iter<true, true, false, 1>(0, A, B);
+            iter<true, true, false, 0>(1, B, A);
             k = 2;
         }
         const int k_last = SMOOTH ? L : L - 1;  // last steady iteration
+        // march rows consumed so far: 1 + 2R (odd), so steady pairs consume
+        // group rows (1, 0) and an odd tail row 1
         for (; k + 1 <= k_last; k += 2) {
-            iter<true, true, true>(k, A, B);
-            iter<true, true, true>(k + 1, B, A);
+            iter<true, true, true, 1>(k, A, B);
+            iter<true, true, true, 0>(k + 1, B, A);
         }
         if (k <= k_last) {  // odd steady count
-            iter<true, true, true>(k, A, B);
+            iter<true, true, true, 1>(k, A, B);
             iter<false, true, true>(k + 1, B, A);
         } else {
+            next_group();  // release the half-consumed last group
             iter<false, true, true>(k, A, B);
         }
     }
@@ -724,9 +686,9 @@ __global__ void __launch_bounds__(WPB * 32, SWE_MINB) swe_step_kernel(const __gr
     __shared__ double s_dt, s_tc;
     __shared__ double s_red[2][WPB];
     SweCtl* ctl = p.ctl;
-    double* stage = reinterpret_cast<double*>(smem_raw) + warp * (D * NF * 32);  // [D][NF][32]
+    double* stage = reinterpret_cast<double*>(smem_raw) + warp * (D * M::SLOT);  // [D][SLOT]
     unsigned long long* bars =
-        reinterpret_cast<unsigned long long*>(reinterpret_cast<double*>(smem_raw) + WPB * D * NF * 32) + warp * D;
+        reinterpret_cast<unsigned long long*>(reinterpret_cast<double*>(smem_raw) + WPB * D * M::SLOT) + warp * D;
 
     if (tid == 0) {
         const volatile SweCtl* vc = ctl;
@@ -782,9 +744,6 @@ __global__ void __launch_bounds__(WPB * 32, SWE_MINB) swe_step_kernel(const __gr
     m.gnn = p.gnn;
     m.pleft = 0;
     m.pdone = false;
-    m.pzsrc = nullptr;
-    m.psrc = nullptr;
-    m.pstep = 0;
     m.pn = 0;
     m.req = 0;
     m.ring = {0, 0u};
@@ -837,7 +796,7 @@ __global__ void __launch_bounds__(WPB * 32, SWE_MINB) swe_step_kernel(const __gr
 
 template <int WPB, bool SMOOTH, bool FLAT>
 constexpr size_t step_smem_bytes() {
-    return static_cast<size_t>(WPB) * kStages * (FLAT ? 3 : 5) * 32 * 8 + WPB * kStages * 8;
+    return static_cast<size_t>(WPB) * kStages * (FLAT ? 3 : 5) * kGroup * 32 * 8 + WPB * kStages * 8;
 }
 
 }  // namespace swe_dev
