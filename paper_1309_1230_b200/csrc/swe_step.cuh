@@ -238,9 +238,11 @@ struct Marcher {
     // per-segment constants
     int i, L, r_start;
     bool in_x, out_x, star_ok, xedge;
+    double* orow;  // output row of the next emit (this lane's column)
     // reductions
     double mx, my;
-    unsigned long long e2, e4, e5;
+    int e2;
+    unsigned long long e4, e5;
 
     __device__ __forceinline__ double shf_nb(double x) const {
         return FWD ? __shfl_down_sync(FULL, x, 1) : __shfl_up_sync(FULL, x, 1);
@@ -328,6 +330,7 @@ struct Marcher {
     }
 
     // output cell: guard (K5), CFL (K6), store, ghosts for the next step (K1)
+    template <bool EDGE>
     __device__ __forceinline__ void emit(const CellVec& o, int rr) {
         const int jj = p.j0 + rr;
         const Rc rc = A::recip(o.h);  // executor.hpp:560-580
@@ -345,10 +348,12 @@ struct Marcher {
         // CFL maxima; a NaN speed (only in a guarded cell) never replaces them
         mx = (sx > mx) ? sx : mx;
         my = (sy > my) ? sy : my;
-        double* row = nxt + static_cast<size_t>(rr + R) * 3 * P + (i + R);
+        double* row = orow;  // == nxt + (rr + R) * 3P + (i + R)
+        orow += S * 3 * P;
         row[0] = o.h;
         row[P] = o.qx;
         row[2 * P] = o.qy;
+        if constexpr (!EDGE) return;
         if (!(xedge || jj == 0 || jj == p.ny - 1)) return;
         if (i == 0) {
             const CellVec g = edge_ghost(SWE_EDGE_W, p.bc[SWE_EDGE_W], o, p.z_w[rr + R], h_min);
@@ -483,7 +488,9 @@ struct Marcher {
     }
 
     // One iteration k of the march: `in` -> `out`.
-    template <bool DO12, bool DO3, bool EMIT, int GI = 0>
+    // EDGE = false: the segment touches no domain edge (interior window, rows
+    // clear of j = 0 and j = ny-1), so every boundary test is compiled out.
+    template <bool EDGE, bool DO12, bool DO3, bool EMIT, int GI = 0>
     __device__ __forceinline__ void iter(int k, const Carry& in, Carry& out) {
         const int b = r_start + S * k;  // stage-2 row (local)
         if constexpr (DO12) {
@@ -522,7 +529,7 @@ struct Marcher {
 
             const int jb = p.j0 + b;
             // dry U* -> row-major first consumer (executor.hpp:429-436, 459-513)
-            if (!(Us.h >= h_min) && star_ok && in_x && jb >= 0 && jb < p.ny) {
+            if (!(Us.h >= h_min) && star_ok && (!EDGE || (in_x && jb >= 0 && jb < p.ny))) {
                 unsigned long long cons;
                 if (FWD) cons = static_cast<unsigned long long>(jb) * p.nx + i;
                 else if (jb >= 1) cons = static_cast<unsigned long long>(jb - 1) * p.nx + i;
@@ -541,7 +548,7 @@ struct Marcher {
             CellVec Hx = {avg(fn_h, Us.qx), avg(fn_qx, FS.fxx), avg(fn_qy, FS.fxy)};
             out.Hyp = {avg(Un.qy, Us.qy), avg(FN.fxy, FS.fxy), avg(FN.gyy, FS.gyy)};
             CellVec hy_a = in.Hyp, hy_b = out.Hyp;  // faces (b-S, b) and (b, b+S)
-            if (xedge || jb == 0 || jb == p.ny - 1) {  // warp-uniform
+            if (EDGE && (xedge || jb == 0 || jb == p.ny - 1)) {  // warp-uniform
                 CellVec xo = {0.0, 0.0, 0.0};
                 int give = 0;
                 boundary_faces(b, jb, U, FU, Us, FS, Hx, hy_a, hy_b, xo, give);
@@ -581,7 +588,7 @@ struct Marcher {
             }
             const int c_row = b - S;
             if constexpr (!SMOOTH) {
-                if (EMIT && out_x) emit(C, c_row);
+                if (EMIT && out_x) emit<EDGE>(C, c_row);
             } else {
                 // smoothing of row q = c - S   (executor.hpp:533-540, scheme.hpp:197-204)
                 const CellVec& Cp = in.Cp;
@@ -595,7 +602,7 @@ struct Marcher {
                         const int jq = p.j0 + q;
                         CellVec cn = FWD ? C : in.Cpp;
                         CellVec cs = FWD ? in.Cpp : C;
-                        if (xedge || jq == 0 || jq == p.ny - 1) {
+                        if (EDGE && (xedge || jq == 0 || jq == p.ny - 1)) {
                             if (i == 0) cw = edge_ghost(SWE_EDGE_W, p.bc[SWE_EDGE_W], Cp, p.z_w[q + R], h_min);
                             if (i == p.nx - 1) ce = edge_ghost(SWE_EDGE_E, p.bc[SWE_EDGE_E], Cp, p.z_e[q + R], h_min);
                             if (jq == 0) cs = edge_ghost(SWE_EDGE_S, p.bc[SWE_EDGE_S], Cp, p.z_s[i], h_min);
@@ -606,7 +613,7 @@ struct Marcher {
                         o.h = Cp.h + nu * (((ce.h - Cp.h) + (cw.h - Cp.h)) + ((cn.h - Cp.h) + (cs.h - Cp.h)));
                         o.qx = Cp.qx + nu * (((ce.qx - Cp.qx) + (cw.qx - Cp.qx)) + ((cn.qx - Cp.qx) + (cs.qx - Cp.qx)));
                         o.qy = Cp.qy + nu * (((ce.qy - Cp.qy) + (cw.qy - Cp.qy)) + ((cn.qy - Cp.qy) + (cs.qy - Cp.qy)));
-                        emit(o, q);
+                        emit<EDGE>(o, q);
                     }
                 }
                 out.Cpp = Cp;
@@ -626,6 +633,14 @@ struct Marcher {
         xedge = (xw0 <= 0) || (xw0 + 31 >= p.nx - 1);
         r_start = FWD ? sg.ra : sg.rb - 1;
 
+        orow = nxt + static_cast<size_t>(r_start + R) * 3 * P + (i + R);  // first output row
+        const int jlo = p.j0 + sg.ra - R - 1, jhi = p.j0 + sg.rb + R;  // rows the march touches, padded
+        if (xedge || jlo <= 0 || jhi >= p.ny - 1) march<true>();
+        else march<false>();
+    }
+
+    template <bool EDGE>
+    __device__ __forceinline__ void march() {
         Carry A, B;
         // pre-iteration: committed row r_start - S*R
         consume<0>(A.U, A.zx, A.zy);  // march row 0
@@ -640,31 +655,31 @@ struct Marcher {
         int k;
         if constexpr (!SMOOTH) {
             // k = -1, 0: no corrector yet; 1..L-1 steady; L: corrector only
-            iter<true, false, false, 1>(-1, A, B);
-            iter<true, false, false, 0>(0, B, A);
+            iter<EDGE, true, false, false, 1>(-1, A, B);
+            iter<EDGE, true, false, false, 0>(0, B, A);
             k = 1;
         } else {
             // k = -2, -1: no corrector; 0, 1: corrector without output;
             // 2..L steady; L+1: corrector + smoothing only
-            iter<true, false, false, 1>(-2, A, B);
-            iter<true, false, false, 0>(-1, B, A);
-            iter<true, true, false, 1>(0, A, B);
-            iter<true, true, false, 0>(1, B, A);
+            iter<EDGE, true, false, false, 1>(-2, A, B);
+            iter<EDGE, true, false, false, 0>(-1, B, A);
+            iter<EDGE, true, true, false, 1>(0, A, B);
+            iter<EDGE, true, true, false, 0>(1, B, A);
             k = 2;
         }
         const int k_last = SMOOTH ? L : L - 1;  // last steady iteration
         // march rows consumed so far: 1 + 2R (odd), so steady pairs consume
         // group rows (1, 0) and an odd tail row 1
         for (; k + 1 <= k_last; k += 2) {
-            iter<true, true, true, 1>(k, A, B);
-            iter<true, true, true, 0>(k + 1, B, A);
+            iter<EDGE, true, true, true, 1>(k, A, B);
+            iter<EDGE, true, true, true, 0>(k + 1, B, A);
         }
         if (k <= k_last) {  // odd steady count
-            iter<true, true, true, 1>(k, A, B);
-            iter<false, true, true>(k + 1, B, A);
+            iter<EDGE, true, true, true, 1>(k, A, B);
+            iter<EDGE, false, true, true>(k + 1, B, A);
         } else {
             next_group();  // release the half-consumed last group
-            iter<false, true, true>(k, A, B);
+            iter<EDGE, false, true, true>(k, A, B);
         }
     }
 };
@@ -749,7 +764,8 @@ __global__ void __launch_bounds__(WPB * 32, SWE_MINB) swe_step_kernel(const __gr
     m.ring = {0, 0u};
     m.mx = 0.0;
     m.my = 0.0;
-    m.e2 = m.e4 = m.e5 = 0ull;
+    m.e2 = 0;
+    m.e4 = m.e5 = 0ull;
     m.produce();
     while (m.qhead < m.qtail) {  // the producer keeps the queue ahead of the consumer
         const Seg sg = m.segq[m.qhead % M::QN];
