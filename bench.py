@@ -205,6 +205,7 @@ def timed_run(sc, kind, nccl_id, args, dist, local, sampler=None):
     torch.cuda.synchronize()
     n0, s0 = stp.timing()
     l0 = stp.launch_count()
+    a0 = stp.activity()["skipped_cells"]
     if sampler:
         sampler.__enter__()
     try:
@@ -213,6 +214,8 @@ def timed_run(sc, kind, nccl_id, args, dist, local, sampler=None):
         if sampler:
             sampler.__exit__()
     torch.cuda.synchronize()
+    act = stp.activity()
+    skipped = act["skipped_cells"] - a0
     n1, s1 = stp.timing()
     launches = stp.launch_count() - l0
     dev_s = s1 - s0
@@ -224,6 +227,7 @@ def timed_run(sc, kind, nccl_id, args, dist, local, sampler=None):
         dev_s = float(t.item())
         dist.barrier()
     stp.close()
+    timed_run.skipped_cells = skipped
     return dev_s, launches, (r1 - r0) * sc.spec.nx
 
 
@@ -302,21 +306,24 @@ def main():
 
     head_exact = bool(args.exact)
     clk = ClockSampler(local)
-    kind = ExecutorKind(exact=head_exact, device=local, rank=rank, nranks=world)
+    early = args.config == "c5"  # wet/dry early-exit tiles (SWE_EXEC_EARLY_EXIT)
+    kind = ExecutorKind(exact=head_exact, device=local, rank=rank, nranks=world, early_exit=early)
     dev_s, launches, cells_local = timed_run(sc, kind, new_id(), args, dist, local, clk)
+    skipped = timed_run.skipped_cells
     total_cells = spec.cell_count()
     value = total_cells * args.steps / dev_s
     ms = dev_s / args.steps * 1e3
 
     other = None
     if not args.fast and not args.exact:  # also report the other arithmetic mode
-        k2 = ExecutorKind(exact=not head_exact, device=local, rank=rank, nranks=world)
+        k2 = ExecutorKind(exact=not head_exact, device=local, rank=rank, nranks=world, early_exit=early)
         d2, l2, _ = timed_run(sc, k2, new_id(), args, dist, local)
         other = {"mode": "exact (-fmad=false, bit-identical to the reference)" if not head_exact else "fast",
                  "value": total_cells * args.steps / d2, "ms_per_step": d2 / args.steps * 1e3,
                  "roofline_frac": round(bpc * cells_local / (d2 / args.steps) / 1e9 / load_peaks()[0], 4)}
 
-    e2e = e2e_run(sc, ExecutorKind(exact=head_exact, device=local), args.e2e_steps) if world == 1 else None
+    e2e = (e2e_run(sc, ExecutorKind(exact=head_exact, device=local, early_exit=early), args.e2e_steps)
+           if world == 1 else None)
 
     peak, peak_src = load_peaks()
     achieved = bpc * cells_local / (ms * 1e-3) / 1e9
@@ -330,6 +337,15 @@ def main():
             "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
             "bytes_per_cell": bpc, "kernel": "swe_step_kernel (fused K1-K6, one launch per step)",
             "achieved_definition": f"{bpc} B/cell-step x {cells_local} cells per launch / mean launch time"}
+    activity = None
+    if early:
+        active = 1.0 - skipped / float(cells_local * args.steps)
+        activity = {"early_exit": True, "active_fraction": round(active, 5),
+                    "skipped_cells": skipped,
+                    "active_cell_steps_per_s": value * active,
+                    "active_roofline_frac": round(achieved * active / peak, 4),
+                    "note": "value/roofline count every interior cell (effective); the active_* figures "
+                            "count only computed (non-skipped) cells"}
 
     cpu = None
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
@@ -353,6 +369,8 @@ def main():
                                      "(CUDA graphs of 64 steps), max over ranks"},
                 "other_mode": other, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk.summary()}
+        if activity:
+            line["activity"] = activity
         print(json.dumps(line))
     if dist:
         dist.destroy_process_group()

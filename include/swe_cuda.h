@@ -103,7 +103,11 @@ enum {
     SWE_EXEC_EXACT = 1u << 0,   /* IEEE expression trees, no FMA contraction:
                                    bit-identical to the reference (the
                                    -fmad=false comparison mode) */
-    SWE_EXEC_NO_GRAPH = 1u << 1 /* advance(): plain launches, no CUDA graph */
+    SWE_EXEC_NO_GRAPH = 1u << 1, /* advance(): plain launches, no CUDA graph */
+    SWE_EXEC_EARLY_EXIT = 1u << 2 /* skip work items whose 3x3 item
+                                     neighbourhood is a flat bed at rest
+                                     (bit-exact: such items are fixed points
+                                     of the step) */
 };
 
 typedef struct swe_exec {
@@ -131,6 +135,14 @@ typedef struct swe_run_result {
     double dt_next;        /* raw CFL dt from the final committed state */
     int32_t guard_warnings;
 } swe_run_result;
+
+/* Early-exit accounting since the last load (SWE_EXEC_EARLY_EXIT). */
+typedef struct swe_activity {
+    uint64_t cells_per_step;  /* interior cells of this rank */
+    uint64_t items_per_step;  /* work items (32-column window x row chunk) */
+    uint64_t eligible_items;  /* interior items on a locally flat bed */
+    uint64_t skipped_cells;   /* cells of skipped items, summed over launches */
+} swe_activity;
 
 /* StepTimings-style device counters (executor.hpp:153-172), CUDA-event based */
 typedef struct swe_timing {
@@ -189,6 +201,8 @@ int swe_cuda_advance(swe_ctx* ctx, double t_end, uint64_t step_index0, double dt
 double swe_cuda_time(const swe_ctx* ctx);
 int32_t swe_cuda_guard_warnings(const swe_ctx* ctx);
 int swe_cuda_timing(const swe_ctx* ctx, swe_timing* out);
+/* Early-exit counters (all zero skips when SWE_EXEC_EARLY_EXIT is off). */
+int swe_cuda_activity(swe_ctx* ctx, swe_activity* out);
 /* Rows owned by this rank: [*row_begin, *row_end). */
 void swe_cuda_rows(const swe_ctx* ctx, int32_t* row_begin, int32_t* row_end);
 /* Committed-halo radius in rows (1 without smoothing, 2 with). */

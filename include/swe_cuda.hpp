@@ -133,6 +133,7 @@ struct ExecutorKind {
     int device = 0;
     bool exact = true;  // -fmad=false expression trees: bit-identical to the reference
     bool graph = true;
+    bool early_exit = false;  // skip quiet items on a flat bed (bit-exact)
     int rank = 0, nranks = 1;
     const void* nccl_id = nullptr;
     static ExecutorKind cuda(int device = 0, bool exact = true) {
@@ -141,7 +142,10 @@ struct ExecutorKind {
         k.exact = exact;
         return k;
     }
-    std::string name() const { return std::string("cuda") + (exact ? "" : ":fast"); }
+    std::string name() const {
+        return std::string("cuda") + (nranks > 1 ? ":" + std::to_string(nranks) : std::string()) +
+               (exact ? "" : ":fast") + (early_exit ? ":early" : "");
+    }
 };
 
 // ---- swe::Stepper ----------------------------------------------------------
@@ -156,7 +160,8 @@ public:
         const swe_boundary_set bs{conv(b.north), conv(b.south), conv(b.east), conv(b.west)};
         swe_exec ex{};
         ex.device = kind.device;
-        ex.flags = (kind.exact ? SWE_EXEC_EXACT : 0u) | (kind.graph ? 0u : SWE_EXEC_NO_GRAPH);
+        ex.flags = (kind.exact ? SWE_EXEC_EXACT : 0u) | (kind.graph ? 0u : SWE_EXEC_NO_GRAPH) |
+                   (kind.early_exit ? SWE_EXEC_EARLY_EXIT : 0u);
         ex.rank = kind.rank;
         ex.nranks = kind.nranks;
         ex.nccl_id = kind.nccl_id;

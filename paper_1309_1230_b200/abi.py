@@ -24,6 +24,7 @@ SWE_BC_FIXED_ETA = 3
 
 SWE_EXEC_EXACT = 1 << 0
 SWE_EXEC_NO_GRAPH = 1 << 1
+SWE_EXEC_EARLY_EXIT = 1 << 2
 
 SWE_NCCL_ID_BYTES = 128
 
@@ -71,6 +72,11 @@ class swe_run_result(C.Structure):
                 ("dt_next", C.c_double), ("guard_warnings", C.c_int32)]
 
 
+class swe_activity(C.Structure):
+    _fields_ = [("cells_per_step", C.c_uint64), ("items_per_step", C.c_uint64),
+                ("eligible_items", C.c_uint64), ("skipped_cells", C.c_uint64)]
+
+
 class swe_timing(C.Structure):
     _fields_ = [("steps", C.c_uint64), ("step_seconds", C.c_double)]
 
@@ -95,6 +101,7 @@ SIGNATURES = {
     "swe_cuda_time": (C.c_double, [C.c_void_p]),
     "swe_cuda_guard_warnings": (C.c_int32, [C.c_void_p]),
     "swe_cuda_timing": (C.c_int, [C.c_void_p, C.POINTER(swe_timing)]),
+    "swe_cuda_activity": (C.c_int, [C.c_void_p, C.POINTER(swe_activity)]),
     "swe_cuda_rows": (None, [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "swe_cuda_halo_rows": (C.c_int32, [C.c_void_p]),
     "swe_cuda_nccl_unique_id": (C.c_int, [C.c_void_p, ST]),

@@ -158,6 +158,44 @@ __global__ void slopes_kernel(const double* zp, double* slope, int P, int R, int
     }
 }
 
+// Early exit, static part: an item (32-column window x row chunk, the step
+// kernel's unit of work) is eligible when its dependency region -- its cells
+// widened by R + 1 <= 3 -- lies inside this rank's own rows and the domain's
+// columns (no ghost or strip-halo cell involved) and the bed slopes of the 3x3
+// block of items around it are all +0.0 (a flat bed, so the rest state
+// (H, +0, +0) is a fixed point of the step).
+__global__ void item_flat_kernel(const double* slope, int P, int R, int nx, int nloc, int TW, int chunk,
+                                 int ntiles, int nitems, unsigned char* flat) {
+    for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+        const int rc = item / ntiles, tile = item % ntiles;
+        const int x0 = tile * TW, x1 = min(x0 + TW, nx), y0 = rc * chunk, y1 = min(y0 + chunk, nloc);
+        const int w = x1 - x0;
+        int bad = 0;
+        for (int k = threadIdx.x; k < (y1 - y0) * w; k += blockDim.x) {
+            const int lr = y0 + k / w, i = x0 + k % w;
+            const size_t o = (static_cast<size_t>(lr + R) * 2) * P + (i + R);
+            bad |= (swe_dev::dbits(slope[o]) | swe_dev::dbits(slope[o + P])) != 0ull;
+        }
+        bad = __syncthreads_or(bad);
+        if (threadIdx.x == 0) flat[item] = bad ? 0 : 1;
+    }
+}
+
+__global__ void item_elig_kernel(const unsigned char* flat, int nx, int nloc, int TW, int chunk, int ntiles,
+                                 int nchunks, int R, unsigned char* elig, unsigned long long* count) {
+    const int nitems = ntiles * nchunks;
+    for (int item = blockIdx.x * blockDim.x + threadIdx.x; item < nitems; item += gridDim.x * blockDim.x) {
+        const int rc = item / ntiles, tile = item % ntiles;
+        const int x0 = tile * TW, x1 = min(x0 + TW, nx), y0 = rc * chunk, y1 = min(y0 + chunk, nloc);
+        const int rad = R + 1;
+        bool ok = x0 - rad >= 0 && x1 + rad <= nx && y0 - rad >= 0 && y1 + rad <= nloc && tile >= 1 &&
+                  tile + 1 < ntiles && rc >= 1 && rc + 1 < nchunks && chunk >= rad && TW >= rad;
+        for (int d = 0; ok && d < 9; ++d) ok = flat[(rc + d / 3 - 1) * ntiles + tile + d % 3 - 1] != 0;
+        elig[item] = ok ? 1 : 0;
+        if (ok) atomicAdd(count, 1ull);
+    }
+}
+
 // Scan words (max-combined, like the step reduction).
 enum { SCAN_BAD = 0, SCAN_MINR = 1, SCAN_GUARD = 2, SCAN_N = 4 };
 
@@ -316,6 +354,15 @@ struct swe_ctx {
     double *d_zw = nullptr, *d_ze = nullptr, *d_zs = nullptr, *d_zn = nullptr;
     unsigned long long* d_scan = nullptr;
     unsigned* d_flags = nullptr;
+    // early exit: quiet flags per buffer, eligibility, per-item flat bits,
+    // counters {skipped cells, eligible items}
+    unsigned long long* d_qflag = nullptr;
+    unsigned char* d_elig = nullptr;
+    unsigned* d_active = nullptr;
+    unsigned char* d_iflat = nullptr;
+    unsigned long long* d_stats = nullptr;
+    int nitems_alloc = 0;
+    bool early = false;
     SweCtl* d_ctl = nullptr;
     SweCtl* h_ctl = nullptr;  // pinned mirror
     std::vector<double> z_host;  // own rows, for state()
@@ -445,7 +492,8 @@ int halo_exchange(swe_ctx* c, int which, swe_status* st) {
 // `cand` = candidate buffer as assumed by the host (used for the strip halo
 // exchange only).
 int enqueue_step(swe_ctx* c, bool fwd, int cand, swe_status* st) {
-    const int v = swe_step_variant(fwd, c->smooth, c->flat, c->manning);
+    const int v = swe_step_variant(fwd, c->smooth, c->flat, c->manning, c->early);
+    if (c->prm.early) CUDA_TRY(swe_launch_schedule(c->exact, c->stream, c->prm));
     CUDA_TRY(swe_launch_step(c->exact, v, c->ncta, c->stream, c->prm));
     ++c->launches;
     if (c->ex.nranks > 1) {
@@ -653,6 +701,7 @@ EXPORT int swe_cuda_create(const swe_grid* grid, const swe_physics* phys, const 
     c->ex = ex;
     c->ex.nccl_id = nullptr;
     c->exact = (ex.flags & SWE_EXEC_EXACT) != 0;
+    c->early = (ex.flags & SWE_EXEC_EARLY_EXIT) != 0;
     c->smooth = phys->nu_art > 0.0;  // StepPlan::standard(nu_art > 0), executor.hpp:730
     c->manning = phys->manning_n > 0.0;
     c->R = c->smooth ? 2 : 1;
@@ -684,6 +733,8 @@ EXPORT int swe_cuda_create(const swe_grid* grid, const swe_physics* phys, const 
     CUDA_TRY(cudaMemsetAsync(c->d_zn, 0, grid->nx * sizeof(double), c->stream));
     CUDA_TRY(cudaMalloc(&c->d_scan, SCAN_N * sizeof(unsigned long long)));
     CUDA_TRY(cudaMalloc(&c->d_flags, 4 * sizeof(unsigned)));
+    CUDA_TRY(cudaMalloc(&c->d_stats, 4 * sizeof(unsigned long long)));
+    CUDA_TRY(cudaMemsetAsync(c->d_stats, 0, 4 * sizeof(unsigned long long), c->stream));
     CUDA_TRY(cudaMalloc(&c->d_ctl, sizeof(SweCtl)));
     CUDA_TRY(cudaMallocHost(&c->h_ctl, sizeof(SweCtl)));
     std::memset(c->h_ctl, 0, sizeof(SweCtl));
@@ -767,6 +818,11 @@ EXPORT void swe_cuda_destroy(swe_ctx* c) {
     cudaFree(c->d_zn);
     cudaFree(c->d_scan);
     cudaFree(c->d_flags);
+    cudaFree(c->d_stats);
+    cudaFree(c->d_qflag);
+    cudaFree(c->d_elig);
+    cudaFree(c->d_iflat);
+    cudaFree(c->d_active);
     cudaFree(c->d_ctl);
     if (c->h_ctl) cudaFreeHost(c->h_ctl);
     if (c->ev0) cudaEventDestroy(c->ev0);
@@ -887,7 +943,7 @@ EXPORT int swe_cuda_load(swe_ctx* c, const double* z, const double* h, const dou
     c->clamp_any = clamp;
 
     // occupancy-sized persistent grid
-    const int v = swe_step_variant(true, c->smooth, c->flat, c->manning);
+    const int v = swe_step_variant(true, c->smooth, c->flat, c->manning, c->early);
     c->occ = swe_step_occupancy(c->exact, v);
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->ex.device);
@@ -905,11 +961,52 @@ EXPORT int swe_cuda_load(swe_ctx* c, const double* z, const double* h, const dou
         const long long workers = ncta * SWE_STEP_WPB;
         long long ch = units / std::max<long long>(1, workers * 16);
         ch = std::max<long long>(16, std::min<long long>(128, ch));
+        // early exit: finer items (32 rows) so the active band is balanced
+        // across workers and skipped at a finer grain
+        if (c->early && c->flat) ch = 32;
         ch = std::min<long long>(ch, nloc);
         c->prm.chunk = static_cast<int>(ch);
         c->prm.nchunks = static_cast<int>((nloc + ch - 1) / ch);
     }
     destroy_graphs(c);  // variant may have changed
+
+    // early-exit tables for this item geometry (flags of both buffers reset:
+    // nothing is known about the candidate buffer after a load)
+    c->prm.early = 0;
+    c->prm.stats = c->d_stats;
+    CUDA_TRY(cudaMemsetAsync(c->d_stats, 0, 4 * sizeof(unsigned long long), c->stream));
+    if (c->early && c->flat) {  // early-exit kernels exist for a flat bed only
+        const int nitems = c->ntiles * c->prm.nchunks;
+        if (nitems != c->nitems_alloc) {
+            cudaFree(c->d_qflag);
+            cudaFree(c->d_elig);
+            cudaFree(c->d_iflat);
+            cudaFree(c->d_active);
+            c->d_qflag = nullptr;
+            c->d_elig = c->d_iflat = nullptr;
+            c->d_active = nullptr;
+            CUDA_TRY(cudaMalloc(&c->d_active, static_cast<size_t>(nitems) * sizeof(unsigned)));
+            CUDA_TRY(cudaMalloc(&c->d_qflag, 2 * static_cast<size_t>(nitems) * sizeof(unsigned long long)));
+            CUDA_TRY(cudaMalloc(&c->d_elig, nitems));
+            CUDA_TRY(cudaMalloc(&c->d_iflat, nitems));
+            c->nitems_alloc = nitems;
+        }
+        CUDA_TRY(cudaMemsetAsync(c->d_qflag, 0, 2 * static_cast<size_t>(nitems) * sizeof(unsigned long long),
+                                 c->stream));
+        const int TW = SWE_TILE_W(R);
+        item_flat_kernel<<<std::min(nitems, 148 * 16), 128, 0, c->stream>>>(c->d_slope, P, R, nx, nloc, TW,
+                                                                             c->prm.chunk, c->ntiles, nitems,
+                                                                             c->d_iflat);
+        CUDA_TRY(cudaGetLastError());
+        item_elig_kernel<<<std::min((nitems + 255) / 256, 148 * 4), 256, 0, c->stream>>>(
+            c->d_iflat, nx, nloc, TW, c->prm.chunk, c->ntiles, c->prm.nchunks, R, c->d_elig, c->d_stats + 1);
+        CUDA_TRY(cudaGetLastError());
+        c->prm.early = 1;
+        c->prm.qflag[0] = c->d_qflag;
+        c->prm.qflag[1] = c->d_qflag + nitems;
+        c->prm.elig = c->d_elig;
+        c->prm.active = c->d_active;
+    }
 
     std::memset(c->h_ctl, 0, sizeof(SweCtl));
     c->h_ctl->t = t;
@@ -1172,6 +1269,21 @@ EXPORT int swe_cuda_timing(const swe_ctx* c, swe_timing* out) {
 EXPORT void swe_cuda_rows(const swe_ctx* c, int32_t* row_begin, int32_t* row_end) {
     if (row_begin) *row_begin = c ? c->j0 : 0;
     if (row_end) *row_end = c ? c->j0 + c->nloc : 0;
+}
+EXPORT int swe_cuda_activity(swe_ctx* c, swe_activity* out) {
+    swe_status* st = nullptr;
+    if (!c || !out) return SWE_ERR_CONFIG;
+    std::memset(out, 0, sizeof *out);
+    if (!c->loaded) return SWE_OK;
+    CUDA_TRY(cudaSetDevice(c->ex.device));
+    unsigned long long v[4];
+    CUDA_TRY(cudaMemcpyAsync(v, c->d_stats, sizeof v, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    out->cells_per_step = static_cast<uint64_t>(c->nloc) * c->g.nx;
+    out->items_per_step = static_cast<uint64_t>(c->ntiles) * c->prm.nchunks;
+    out->eligible_items = v[1];
+    out->skipped_cells = v[0];
+    return SWE_OK;
 }
 EXPORT int32_t swe_cuda_halo_rows(const swe_ctx* c) { return c ? c->R : 0; }
 EXPORT uint64_t swe_cuda_launch_count(const swe_ctx* c) { return c ? c->launches : 0; }

@@ -12,17 +12,23 @@
 #define SWE_TILE_W(R) (32 - 2 * (R))  // output columns per warp window
 #define SWE_ROW_GROUP 2               // rows per TMA request (state box 32 x 3G, slope box 32 x 2G)
 
-inline int swe_step_variant(bool fwd, bool smooth, bool flat, bool manning) {
-    return (fwd ? 8 : 0) | (smooth ? 4 : 0) | (flat ? 2 : 0) | (manning ? 1 : 0);
+// bit 16: early-exit instantiation (flat bed only)
+inline int swe_step_variant(bool fwd, bool smooth, bool flat, bool manning, bool early = false) {
+    return (fwd ? 8 : 0) | (smooth ? 4 : 0) | (flat ? 2 : 0) | (manning ? 1 : 0) | ((early && flat) ? 16 : 0);
 }
 cudaError_t swe_launch_step_exact(int variant, int grid, cudaStream_t stream, const StepParams& p);
 cudaError_t swe_launch_step_fast(int variant, int grid, cudaStream_t stream, const StepParams& p);
 int swe_step_occupancy_exact(int variant);
 int swe_step_occupancy_fast(int variant);
+cudaError_t swe_launch_schedule_exact(cudaStream_t stream, const StepParams& p);
+cudaError_t swe_launch_schedule_fast(cudaStream_t stream, const StepParams& p);
 cudaError_t swe_launch_finalize(cudaStream_t stream, const StepParams& p);
 
 inline cudaError_t swe_launch_step(bool exact, int variant, int grid, cudaStream_t stream, const StepParams& p) {
     return exact ? swe_launch_step_exact(variant, grid, stream, p) : swe_launch_step_fast(variant, grid, stream, p);
+}
+inline cudaError_t swe_launch_schedule(bool exact, cudaStream_t stream, const StepParams& p) {
+    return exact ? swe_launch_schedule_exact(stream, p) : swe_launch_schedule_fast(stream, p);
 }
 inline int swe_step_occupancy(bool exact, int variant) {
     return exact ? swe_step_occupancy_exact(variant) : swe_step_occupancy_fast(variant);

@@ -172,6 +172,7 @@ __device__ __forceinline__ void finalize_step(const StepParams& p, SweCtl* c, do
     for (int k = 0; k < RED_N; ++k) red[k] = 0ull;
     c->finish = 0u;
     c->work = 0u;
+    c->nactive = 0u;
     __threadfence();
 }
 
@@ -205,7 +206,7 @@ struct WarpRing {  // per-warp TMA ring state (warp-uniform)
     unsigned ph;   // its mbarrier phase parity
 };
 
-template <int WPB, bool FWD, bool SMOOTH, bool FLAT, bool MANNING, bool EXACT>
+template <int WPB, bool FWD, bool SMOOTH, bool FLAT, bool MANNING, bool EXACT, bool EARLY>
 struct Marcher {
     using A = Arith<EXACT>;
     using Rc = typename A::Rc;
@@ -243,6 +244,11 @@ struct Marcher {
     double mx, my;
     int e2;
     unsigned long long e4, e5;
+    // quiet-item tracking of the current segment (early exit): with
+    // mom = bits(qx) | bits(qy) per output cell, qo |= bits(h) | mom and
+    // qn &= bits(h) & ~mom end equal iff every cell is (H, +0, +0), same H
+    unsigned long long qo, qn;
+    unsigned nitems;  // items of this launch (all, or the active list)
 
     __device__ __forceinline__ double shf_nb(double x) const {
         return FWD ? __shfl_down_sync(FULL, x, 1) : __shfl_up_sync(FULL, x, 1);
@@ -262,16 +268,18 @@ struct Marcher {
     // atomic counter, queue it for the consumer and point this lane at its
     // first row.  Dynamic claiming balances the cheaper interior windows
     // against the boundary windows and any per-SM speed differences.
+    // With EARLY the items come from the active list the schedule kernel
+    // built for this step (quiet items already accounted for).
     __device__ __forceinline__ void prod_seg() {
         unsigned item = 0;
         if (lane == 0) item = atomicAdd(&p.ctl->work, 1u);
         item = __shfl_sync(FULL, item, 0);
-        const unsigned nitems = static_cast<unsigned>(p.ntiles) * static_cast<unsigned>(p.nchunks);
         if (item >= nitems) {
             pleft = 0;
             pdone = true;
             return;
         }
+        if constexpr (EARLY) item = p.active[item];
         const int rc = static_cast<int>(item / p.ntiles);   // row-chunk major: neighbouring
         const int tile = static_cast<int>(item % p.ntiles); // windows share halo sectors in L2
         Seg sg;
@@ -348,6 +356,11 @@ struct Marcher {
         // CFL maxima; a NaN speed (only in a guarded cell) never replaces them
         mx = (sx > mx) ? sx : mx;
         my = (sy > my) ? sy : my;
+        if constexpr (EARLY) {
+            const unsigned long long hb = dbits(o.h), mom = dbits(o.qx) | dbits(o.qy);
+            qo |= hb | mom;
+            qn &= hb & ~mom;
+        }
         double* row = orow;  // == nxt + (rr + R) * 3P + (i + R)
         orow += S * 3 * P;
         row[0] = o.h;
@@ -634,9 +647,21 @@ struct Marcher {
         r_start = FWD ? sg.ra : sg.rb - 1;
 
         orow = nxt + static_cast<size_t>(r_start + R) * 3 * P + (i + R);  // first output row
+        qo = 0ull;
+        qn = ~0ull;
         const int jlo = p.j0 + sg.ra - R - 1, jhi = p.j0 + sg.rb + R;  // rows the march touches, padded
         if (xedge || jlo <= 0 || jhi >= p.ny - 1) march<true>();
         else march<false>();
+        if constexpr (EARLY) {
+            // quiet flag of this item in the candidate buffer: the depth bits
+            // H when every output cell is (H, +0, +0) with H >= h_min, else 0
+            const unsigned long long ref = __shfl_sync(FULL, qo, R);  // lane R is always an output lane
+            const bool ok = !out_x || (qo == qn && qo == ref);
+            const double H = __longlong_as_double(static_cast<long long>(ref));
+            const bool quiet = __all_sync(FULL, ok) && H >= h_min && finite_d(H);
+            if (lane == 0)
+                p.qflag[sel ^ 1][(sg.ra / p.chunk) * p.ntiles + sg.tile] = quiet ? ref : 0ull;
+        }
     }
 
     template <bool EDGE>
@@ -684,9 +709,9 @@ struct Marcher {
     }
 };
 
-template <int WPB, bool FWD, bool SMOOTH, bool FLAT, bool MANNING, bool EXACT>
+template <int WPB, bool FWD, bool SMOOTH, bool FLAT, bool MANNING, bool EXACT, bool EARLY>
 __global__ void __launch_bounds__(WPB * 32, SWE_MINB) swe_step_kernel(const __grid_constant__ StepParams p) {
-    using M = Marcher<WPB, FWD, SMOOTH, FLAT, MANNING, EXACT>;
+    using M = Marcher<WPB, FWD, SMOOTH, FLAT, MANNING, EXACT, EARLY>;
     constexpr int D = kStages;
     constexpr int NF = M::NF;
     constexpr unsigned FULL = 0xffffffffu;
@@ -698,6 +723,7 @@ __global__ void __launch_bounds__(WPB * 32, SWE_MINB) swe_step_kernel(const __gr
 
     __shared__ Seg segq_all[WPB][M::QN];
     __shared__ int s_skip, s_sel, s_last;
+    __shared__ unsigned s_nact;
     __shared__ double s_dt, s_tc;
     __shared__ double s_red[2][WPB];
     SweCtl* ctl = p.ctl;
@@ -726,6 +752,7 @@ __global__ void __launch_bounds__(WPB * 32, SWE_MINB) swe_step_kernel(const __gr
         s_dt = dt;
         s_tc = tc;
         s_sel = vc->sel;
+        s_nact = EARLY ? vc->nactive : 0u;
     }
     if (lane == 0) {
         for (int d = 0; d < D; ++d) mbar_init(&bars[d], 1);
@@ -766,6 +793,9 @@ __global__ void __launch_bounds__(WPB * 32, SWE_MINB) swe_step_kernel(const __gr
     m.my = 0.0;
     m.e2 = 0;
     m.e4 = m.e5 = 0ull;
+    m.nitems = EARLY ? s_nact : static_cast<unsigned>(p.ntiles) * static_cast<unsigned>(p.nchunks);
+    m.qo = 0ull;
+    m.qn = ~0ull;
     m.produce();
     while (m.qhead < m.qtail) {  // the producer keeps the queue ahead of the consumer
         const Seg sg = m.segq[m.qhead % M::QN];
@@ -807,6 +837,86 @@ __global__ void __launch_bounds__(WPB * 32, SWE_MINB) swe_step_kernel(const __gr
     if (s_last && tid == 0) {
         __threadfence();
         finalize_step(p, ctl, s_dt, s_tc);
+    }
+}
+
+// ------------------------------------------------------------ early exit
+// Schedule kernel (Brodtkorb-style early-exit tiles), run
+// before each early-exit step.  An eligible item (interior, flat bed over its
+// 3x3 item neighbourhood; see item_elig_kernel) is skipped when all 9 items
+// its output depends on (dependency radius R + 1 <= 3 < item size) are quiet
+// with the same depth H in the committed buffer -- a flat bed at rest, a
+// bit-exact fixed point of the step -- and the candidate buffer already holds
+// that same quiet item.  Skipped items contribute their CFL speed
+// sqrt(g H) (u = v = 0, exactly as the step's epilogue computes it) to the
+// reduction words; the others are appended to the step's active list.
+template <bool EXACT>
+__global__ void __launch_bounds__(256) swe_schedule_kernel(const __grid_constant__ StepParams p) {
+    SweCtl* ctl = p.ctl;
+    __shared__ int s_go, s_sel;
+    __shared__ double s_max[8];
+    __shared__ unsigned long long s_cells[8];
+    if (threadIdx.x == 0) {
+        const volatile SweCtl* vc = ctl;
+        int go = !vc->done;
+        if (go && vc->mode == 1 && !(vc->t < vc->t_end)) go = 0;  // same no-op rule as the step
+        s_go = go;
+        s_sel = vc->sel;
+    }
+    __syncthreads();
+    if (!s_go) return;
+    const int sel = s_sel;
+    const unsigned nitems = static_cast<unsigned>(p.ntiles) * static_cast<unsigned>(p.nchunks);
+    const int tw = 32 - 2 * (p.nu > 0.0 ? 2 : 1);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double smax = 0.0;
+    unsigned long long cells = 0ull;
+    const unsigned stride = gridDim.x * blockDim.x;
+    for (unsigned base = blockIdx.x * blockDim.x; base < nitems; base += stride) {
+        const unsigned item = base + threadIdx.x;
+        bool skip = false;
+        if (item < nitems && p.elig[item]) {
+            const int rc = static_cast<int>(item / p.ntiles), tile = static_cast<int>(item % p.ntiles);
+            const unsigned long long c = p.qflag[sel][item];
+            skip = c != 0ull && p.qflag[sel ^ 1][item] == c;
+            for (int d = 0; skip && d < 9; ++d)
+                skip = p.qflag[sel][(rc + d / 3 - 1) * p.ntiles + tile + d % 3 - 1] == c;
+            if (skip) {
+                const double s = Arith<EXACT>::sqrt_(p.g * __longlong_as_double(static_cast<long long>(c)));
+                smax = (s > smax) ? s : smax;
+                const int ra = rc * p.chunk, rb = min(ra + p.chunk, p.nloc);
+                const int x0 = tile * tw, x1 = min(x0 + tw, p.nx);
+                cells += static_cast<unsigned long long>(rb - ra) * static_cast<unsigned long long>(x1 - x0);
+            }
+        }
+        const bool act = item < nitems && !skip;
+        const unsigned ball = __ballot_sync(0xffffffffu, act);
+        unsigned pos = 0;
+        if (lane == 0 && ball) pos = atomicAdd(&ctl->nactive, static_cast<unsigned>(__popc(ball)));
+        pos = __shfl_sync(0xffffffffu, pos, 0);
+        if (act) p.active[pos + __popc(ball & ((1u << lane) - 1u))] = item;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        smax = fmax(smax, __shfl_xor_sync(0xffffffffu, smax, o));
+        cells += __shfl_xor_sync(0xffffffffu, cells, o);
+    }
+    if (lane == 0) {
+        s_max[warp] = smax;
+        s_cells[warp] = cells;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double m = 0.0;
+        unsigned long long n = 0ull;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+            m = fmax(m, s_max[w]);
+            n += s_cells[w];
+        }
+        if (n) {  // sx = sy = sqrt(g H) for a quiet cell
+            atomicMax(&ctl->red[RED_SX], dbits(m));
+            atomicMax(&ctl->red[RED_SY], dbits(m));
+            atomicAdd(&p.stats[0], n);
+        }
     }
 }
 

@@ -6,6 +6,7 @@
 //     the step is bit-identical to the reference built with -ffp-contract=off;
 //   SWE_EXACT_TU=0 with -fmad=true: FMA contraction + shared reciprocals
 //     (tolerance parity).
+#include <algorithm>
 #include <cstdio>
 
 #include "swe_launch.h"
@@ -20,10 +21,10 @@ namespace {
 constexpr int kWPB = SWE_STEP_WPB;  // warps (independent workers) per CTA
 constexpr bool kExact = SWE_EXACT_TU != 0;
 
-template <bool FWD, bool SMOOTH, bool FLAT, bool MANNING>
+template <bool FWD, bool SMOOTH, bool FLAT, bool MANNING, bool EARLY = false>
 cudaError_t launch_one(int grid, cudaStream_t s, const StepParams& p) {
     constexpr size_t smem = swe_dev::step_smem_bytes<kWPB, SMOOTH, FLAT>();
-    auto k = swe_dev::swe_step_kernel<kWPB, FWD, SMOOTH, FLAT, MANNING, kExact>;
+    auto k = swe_dev::swe_step_kernel<kWPB, FWD, SMOOTH, FLAT, MANNING, kExact, EARLY>;
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -35,10 +36,10 @@ cudaError_t launch_one(int grid, cudaStream_t s, const StepParams& p) {
     return cudaGetLastError();
 }
 
-template <bool FWD, bool SMOOTH, bool FLAT, bool MANNING>
+template <bool FWD, bool SMOOTH, bool FLAT, bool MANNING, bool EARLY = false>
 int occupancy_one() {
     constexpr size_t smem = swe_dev::step_smem_bytes<kWPB, SMOOTH, FLAT>();
-    auto k = swe_dev::swe_step_kernel<kWPB, FWD, SMOOTH, FLAT, MANNING, kExact>;
+    auto k = swe_dev::swe_step_kernel<kWPB, FWD, SMOOTH, FLAT, MANNING, kExact, EARLY>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     int n = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kWPB * 32, smem) != cudaSuccess) return 1;
@@ -63,15 +64,35 @@ const Entry kTable[16] = {
     SWE_V(true, true, false, false),   SWE_V(true, true, false, true),
     SWE_V(true, true, true, false),    SWE_V(true, true, true, true),
 };
+// early-exit variants exist for a flat bed only (variant bit 16)
+#define SWE_E(F, S, M) {launch_one<F, S, true, M, true>, occupancy_one<F, S, true, M, true>}
+const Entry kTableEarly[8] = {
+    SWE_E(false, false, false), SWE_E(false, false, true), SWE_E(false, true, false), SWE_E(false, true, true),
+    SWE_E(true, false, false),  SWE_E(true, false, true),  SWE_E(true, true, false),  SWE_E(true, true, true),
+};
+#undef SWE_E
 #undef SWE_V
+
+static const Entry& entry(int variant) {
+    if (variant & 16) return kTableEarly[((variant >> 1) & 4) | ((variant >> 1) & 2) | (variant & 1)];
+    return kTable[variant & 15];
+}
 
 }  // namespace
 
-#if SWE_EXACT_TU
-cudaError_t swe_launch_step_exact(int variant, int grid, cudaStream_t stream, const StepParams& p) {
-    return kTable[variant & 15].launch(grid, stream, p);
+static cudaError_t launch_schedule(cudaStream_t stream, const StepParams& p) {
+    const int items = p.ntiles * p.nchunks;
+    const int grid = std::max(1, std::min((items + 255) / 256, 148 * 4));
+    swe_dev::swe_schedule_kernel<kExact><<<grid, 256, 0, stream>>>(p);
+    return cudaGetLastError();
 }
-int swe_step_occupancy_exact(int variant) { return kTable[variant & 15].occ(); }
+
+#if SWE_EXACT_TU
+cudaError_t swe_launch_schedule_exact(cudaStream_t stream, const StepParams& p) { return launch_schedule(stream, p); }
+cudaError_t swe_launch_step_exact(int variant, int grid, cudaStream_t stream, const StepParams& p) {
+    return entry(variant).launch(grid, stream, p);
+}
+int swe_step_occupancy_exact(int variant) { return entry(variant).occ(); }
 
 __global__ void swe_finalize_kernel(const __grid_constant__ StepParams p) {
     SweCtl* c = p.ctl;
@@ -97,8 +118,9 @@ cudaError_t swe_launch_finalize(cudaStream_t stream, const StepParams& p) {
     return cudaGetLastError();
 }
 #else
+cudaError_t swe_launch_schedule_fast(cudaStream_t stream, const StepParams& p) { return launch_schedule(stream, p); }
 cudaError_t swe_launch_step_fast(int variant, int grid, cudaStream_t stream, const StepParams& p) {
-    return kTable[variant & 15].launch(grid, stream, p);
+    return entry(variant).launch(grid, stream, p);
 }
-int swe_step_occupancy_fast(int variant) { return kTable[variant & 15].occ(); }
+int swe_step_occupancy_fast(int variant) { return entry(variant).occ(); }
 #endif

@@ -52,6 +52,7 @@ struct __align__(16) SweCtl {
     int err_i, err_j;
     unsigned int finish;          // CTA arrival counter for the last-block finalize
     unsigned int work;            // dynamic work-item counter of the step kernel
+    unsigned int nactive;         // early exit: length of the step's active item list
     unsigned long long red[RED_N];
 };
 
@@ -70,6 +71,15 @@ struct StepParams {
     const double* z_s;     // bed z at global row 0 per column
     const double* z_n;     // bed z at global row ny-1 per column
     SweCtl* ctl;
+    // early exit (SWE_EXEC_EARLY_EXIT): per-buffer quiet flags of the work
+    // items (depth bits H of an all-(H, +0, +0) item, else 0), static
+    // eligibility (interior item, flat bed over its 3x3 neighbourhood), and
+    // counters {skipped cells}
+    unsigned long long* qflag[2];
+    const unsigned char* elig;
+    unsigned* active;      // active item list (schedule kernel -> step kernel)
+    unsigned long long* stats;
+    int early;
     int nx, ny;            // global grid
     int nloc, j0;          // rows owned by this rank: global [j0, j0+nloc)
     int pitch;             // doubles per field row (P)

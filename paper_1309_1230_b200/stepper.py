@@ -189,9 +189,11 @@ class ExecutorKind:
     graph: bool = True
     rank: int = 0
     nranks: int = 1
+    early_exit: bool = False  # skip quiet items on a flat bed (bit-exact; SWE_EXEC_EARLY_EXIT)
 
     def name(self):
-        return "cuda" + ("" if self.nranks == 1 else f":{self.nranks}") + ("" if self.exact else ":fast")
+        return ("cuda" + ("" if self.nranks == 1 else f":{self.nranks}") + ("" if self.exact else ":fast")
+                + (":early" if self.early_exit else ""))
 
 
 def _bc(bk: BoundaryKind) -> abi.swe_boundary:
@@ -209,7 +211,8 @@ class Stepper:
         p = abi.swe_physics(phys.g, phys.manning_n, phys.nu_art)
         po = abi.swe_policy(pol.cfl, pol.dt_max, pol.dt_min, pol.h_min)
         b = abi.swe_boundary_set(_bc(bounds.north), _bc(bounds.south), _bc(bounds.east), _bc(bounds.west))
-        flags = (abi.SWE_EXEC_EXACT if kind.exact else 0) | (0 if kind.graph else abi.SWE_EXEC_NO_GRAPH)
+        flags = ((abi.SWE_EXEC_EXACT if kind.exact else 0) | (0 if kind.graph else abi.SWE_EXEC_NO_GRAPH)
+                 | (abi.SWE_EXEC_EARLY_EXIT if kind.early_exit else 0))
         self._id_buf = C.create_string_buffer(nccl_id, abi.SWE_NCCL_ID_BYTES) if nccl_id else None
         ex = abi.swe_exec(kind.device, flags, kind.rank, kind.nranks,
                           C.cast(self._id_buf, C.c_void_p) if self._id_buf is not None else None)
@@ -329,6 +332,13 @@ class Stepper:
         t = abi.swe_timing()
         self._lib.swe_cuda_timing(self._ctx, C.byref(t))
         return t.steps, t.step_seconds
+
+    def activity(self) -> dict:
+        """Early-exit counters since the last load (swe_cuda_activity)."""
+        a = abi.swe_activity()
+        self._lib.swe_cuda_activity(self._ctx, C.byref(a))
+        return {"cells_per_step": a.cells_per_step, "items_per_step": a.items_per_step,
+                "eligible_items": a.eligible_items, "skipped_cells": a.skipped_cells}
 
     def halo_rows(self) -> int:
         return self._lib.swe_cuda_halo_rows(self._ctx)
