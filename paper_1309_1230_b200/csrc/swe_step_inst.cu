@@ -1,11 +1,16 @@
-// swe_step_inst.cu — instantiations of the fused step kernel and a launcher
-// table indexed by (sweep parity, smoothing, flat bed, Manning friction).
+// swe_step_inst.cu — instantiations of the fused step kernel, one slice of the
+// variant space per translation unit so the build runs in parallel.
 //
-// Compiled twice (see __graft_entry__.build):
-//   SWE_EXACT_TU=1 with -fmad=false: expression trees are never contracted, so
-//     the step is bit-identical to the reference built with -ffp-contract=off;
-//   SWE_EXACT_TU=0 with -fmad=true: FMA contraction + shared reciprocals
-//     (tolerance parity).
+// Compiled 8 times (see __graft_entry__.build):
+//   SWE_EXACT_TU = 1 / 0   exact (IEEE expression trees, bit-identical to the
+//                          reference built with -ffp-contract=off) / fast
+//                          (explicit FMA + shared reciprocals, tolerance parity)
+//                          -- both with -fmad=false; fast mode writes its FMAs
+//                          explicitly;
+//   SWE_PART = 0..3        sweep parity (bit 1) x smoothing (bit 0).
+// Each part instantiates flat/sloped x frictionless/Manning, plus the
+// early-exit kernels (flat bed only).  Part 0 also carries the schedule and
+// finalize kernels of its mode.
 #include <algorithm>
 #include <cstdio>
 
@@ -15,16 +20,28 @@
 #ifndef SWE_EXACT_TU
 #define SWE_EXACT_TU 1
 #endif
+#ifndef SWE_PART
+#define SWE_PART 0
+#endif
 
-namespace {
+#define SWE_CAT2(a, b) a##b
+#define SWE_CAT(a, b) SWE_CAT2(a, b)
+#define SWE_MODE_NAME(x) SWE_CAT(SWE_CAT(x, SWE_PART), SWE_CAT(_, SWE_EXACT_TU))
+
+// One uniquely named namespace per (part, mode): the same source is compiled
+// 8 times, and nvcc names an anonymous namespace after the file, so internal
+// helpers of different TUs would otherwise share (and merge) symbol names.
+namespace SWE_MODE_NAME(swe_inst) {
 
 constexpr int kWPB = SWE_STEP_WPB;  // warps (independent workers) per CTA
 constexpr bool kExact = SWE_EXACT_TU != 0;
+constexpr bool kFwd = (SWE_PART & 2) != 0;
+constexpr bool kSmooth = (SWE_PART & 1) != 0;
 
-template <bool FWD, bool SMOOTH, bool FLAT, bool MANNING, bool EARLY = false>
+template <bool FLAT, bool MANNING, bool EARLY>
 cudaError_t launch_one(int grid, cudaStream_t s, const StepParams& p) {
-    constexpr size_t smem = swe_dev::step_smem_bytes<kWPB, SMOOTH, FLAT>();
-    auto k = swe_dev::swe_step_kernel<kWPB, FWD, SMOOTH, FLAT, MANNING, kExact, EARLY>;
+    constexpr size_t smem = swe_dev::step_smem_bytes<kWPB, kSmooth, FLAT>();
+    auto k = swe_dev::swe_step_kernel<kWPB, kFwd, kSmooth, FLAT, MANNING, kExact, EARLY>;
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -36,10 +53,10 @@ cudaError_t launch_one(int grid, cudaStream_t s, const StepParams& p) {
     return cudaGetLastError();
 }
 
-template <bool FWD, bool SMOOTH, bool FLAT, bool MANNING, bool EARLY = false>
+template <bool FLAT, bool MANNING, bool EARLY>
 int occupancy_one() {
-    constexpr size_t smem = swe_dev::step_smem_bytes<kWPB, SMOOTH, FLAT>();
-    auto k = swe_dev::swe_step_kernel<kWPB, FWD, SMOOTH, FLAT, MANNING, kExact, EARLY>;
+    constexpr size_t smem = swe_dev::step_smem_bytes<kWPB, kSmooth, FLAT>();
+    auto k = swe_dev::swe_step_kernel<kWPB, kFwd, kSmooth, FLAT, MANNING, kExact, EARLY>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     int n = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kWPB * 32, smem) != cudaSuccess) return 1;
@@ -48,51 +65,63 @@ int occupancy_one() {
 
 using LaunchFn = cudaError_t (*)(int, cudaStream_t, const StepParams&);
 using OccFn = int (*)();
-
 struct Entry {
     LaunchFn launch;
     OccFn occ;
 };
-#define SWE_V(F, S, Z, M) {launch_one<F, S, Z, M>, occupancy_one<F, S, Z, M>}
-const Entry kTable[16] = {
-    SWE_V(false, false, false, false), SWE_V(false, false, false, true),
-    SWE_V(false, false, true, false),  SWE_V(false, false, true, true),
-    SWE_V(false, true, false, false),  SWE_V(false, true, false, true),
-    SWE_V(false, true, true, false),   SWE_V(false, true, true, true),
-    SWE_V(true, false, false, false),  SWE_V(true, false, false, true),
-    SWE_V(true, false, true, false),   SWE_V(true, false, true, true),
-    SWE_V(true, true, false, false),   SWE_V(true, true, false, true),
-    SWE_V(true, true, true, false),    SWE_V(true, true, true, true),
-};
-// early-exit variants exist for a flat bed only (variant bit 16)
-#define SWE_E(F, S, M) {launch_one<F, S, true, M, true>, occupancy_one<F, S, true, M, true>}
-const Entry kTableEarly[8] = {
-    SWE_E(false, false, false), SWE_E(false, false, true), SWE_E(false, true, false), SWE_E(false, true, true),
-    SWE_E(true, false, false),  SWE_E(true, false, true),  SWE_E(true, true, false),  SWE_E(true, true, true),
-};
-#undef SWE_E
+#define SWE_V(Z, M, E) {launch_one<Z, M, E>, occupancy_one<Z, M, E>}
+// index: flat (bit 1) | manning (bit 0); early-exit kernels exist for a flat bed only
+const Entry kTable[4] = {SWE_V(false, false, false), SWE_V(false, true, false), SWE_V(true, false, false),
+                         SWE_V(true, true, false)};
+const Entry kEarly[2] = {SWE_V(true, false, true), SWE_V(true, true, true)};
 #undef SWE_V
 
-static const Entry& entry(int variant) {
-    if (variant & 16) return kTableEarly[((variant >> 1) & 4) | ((variant >> 1) & 2) | (variant & 1)];
-    return kTable[variant & 15];
+const Entry& entry(int variant) { return (variant & 16) ? kEarly[variant & 1] : kTable[variant & 3]; }
+
+}  // namespace swe_inst<part>_<mode>
+using namespace SWE_MODE_NAME(swe_inst);
+
+// per-part entry points, dispatched by swe_launch_step_{exact,fast} below
+cudaError_t SWE_MODE_NAME(swe_part_launch)(int variant, int grid, cudaStream_t stream, const StepParams& p) {
+    return entry(variant).launch(grid, stream, p);
 }
+int SWE_MODE_NAME(swe_part_occ)(int variant) { return entry(variant).occ(); }
 
-}  // namespace
+#if SWE_PART == 0
+// declarations of the other parts of this mode
+#define SWE_DECL(k)                                                                                         \
+    cudaError_t SWE_CAT(SWE_CAT(swe_part_launch, k), SWE_CAT(_, SWE_EXACT_TU))(int, int, cudaStream_t,      \
+                                                                               const StepParams&);         \
+    int SWE_CAT(SWE_CAT(swe_part_occ, k), SWE_CAT(_, SWE_EXACT_TU))(int);
+SWE_DECL(1)
+SWE_DECL(2)
+SWE_DECL(3)
+#undef SWE_DECL
 
-static cudaError_t launch_schedule(cudaStream_t stream, const StepParams& p) {
+namespace SWE_MODE_NAME(swe_inst) {
+using PartLaunch = cudaError_t (*)(int, int, cudaStream_t, const StepParams&);
+using PartOcc = int (*)(int);
+const PartLaunch kPartLaunch[4] = {SWE_CAT(swe_part_launch0_, SWE_EXACT_TU), SWE_CAT(swe_part_launch1_, SWE_EXACT_TU),
+                                   SWE_CAT(swe_part_launch2_, SWE_EXACT_TU), SWE_CAT(swe_part_launch3_, SWE_EXACT_TU)};
+const PartOcc kPartOcc[4] = {SWE_CAT(swe_part_occ0_, SWE_EXACT_TU), SWE_CAT(swe_part_occ1_, SWE_EXACT_TU),
+                             SWE_CAT(swe_part_occ2_, SWE_EXACT_TU), SWE_CAT(swe_part_occ3_, SWE_EXACT_TU)};
+// swe_step_variant bits: fwd 8, smooth 4, flat 2, manning 1, early 16
+int part_of(int variant) { return ((variant >> 3) & 1) * 2 + ((variant >> 2) & 1); }
+
+cudaError_t launch_schedule(cudaStream_t stream, const StepParams& p) {
     const int items = p.ntiles * p.nchunks;
     const int grid = std::max(1, std::min((items + 255) / 256, 148 * 4));
     swe_dev::swe_schedule_kernel<kExact><<<grid, 256, 0, stream>>>(p);
     return cudaGetLastError();
 }
+}  // namespace swe_inst<part>_<mode>
 
 #if SWE_EXACT_TU
-cudaError_t swe_launch_schedule_exact(cudaStream_t stream, const StepParams& p) { return launch_schedule(stream, p); }
 cudaError_t swe_launch_step_exact(int variant, int grid, cudaStream_t stream, const StepParams& p) {
-    return entry(variant).launch(grid, stream, p);
+    return kPartLaunch[part_of(variant)](variant, grid, stream, p);
 }
-int swe_step_occupancy_exact(int variant) { return entry(variant).occ(); }
+int swe_step_occupancy_exact(int variant) { return kPartOcc[part_of(variant)](variant); }
+cudaError_t swe_launch_schedule_exact(cudaStream_t stream, const StepParams& p) { return launch_schedule(stream, p); }
 
 __global__ void swe_finalize_kernel(const __grid_constant__ StepParams p) {
     SweCtl* c = p.ctl;
@@ -118,9 +147,10 @@ cudaError_t swe_launch_finalize(cudaStream_t stream, const StepParams& p) {
     return cudaGetLastError();
 }
 #else
-cudaError_t swe_launch_schedule_fast(cudaStream_t stream, const StepParams& p) { return launch_schedule(stream, p); }
 cudaError_t swe_launch_step_fast(int variant, int grid, cudaStream_t stream, const StepParams& p) {
-    return entry(variant).launch(grid, stream, p);
+    return kPartLaunch[part_of(variant)](variant, grid, stream, p);
 }
-int swe_step_occupancy_fast(int variant) { return entry(variant).occ(); }
+int swe_step_occupancy_fast(int variant) { return kPartOcc[part_of(variant)](variant); }
+cudaError_t swe_launch_schedule_fast(cudaStream_t stream, const StepParams& p) { return launch_schedule(stream, p); }
 #endif
+#endif  // SWE_PART == 0

@@ -4,9 +4,12 @@ set -e
 name=$1; shift
 out=build/var_$name; mkdir -p $out
 NV="/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-fvisibility=hidden"
-$NV -fmad=false -DSWE_EXACT_TU=1 "$@" -c paper_1309_1230_b200/csrc/swe_step_inst.cu -o $out/e.o &
-$NV -fmad=false -DSWE_EXACT_TU=0 "$@" -c paper_1309_1230_b200/csrc/swe_step_inst.cu -o $out/f.o &
+objs=""
+for e in 1 0; do for k in 0 1 2 3; do
+$NV -fmad=false -DSWE_EXACT_TU=$e -DSWE_PART=$k "$@" -c paper_1309_1230_b200/csrc/swe_step_inst.cu -o $out/s${e}${k}.o &
+objs="$objs $out/s${e}${k}.o"
+done; done
 $NV -fmad=false "$@" -c paper_1309_1230_b200/csrc/swe_capi.cu -o $out/c.o &
 wait
-/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o paper_1309_1230_b200/lib/libswe_cuda_$name.so $out/e.o $out/f.o $out/c.o -lcudart -ldl
+/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o paper_1309_1230_b200/lib/libswe_cuda_$name.so $objs $out/c.o -lcudart -ldl
 echo built paper_1309_1230_b200/lib/libswe_cuda_$name.so
