@@ -104,10 +104,17 @@ enum {
                                    bit-identical to the reference (the
                                    -fmad=false comparison mode) */
     SWE_EXEC_NO_GRAPH = 1u << 1, /* advance(): plain launches, no CUDA graph */
-    SWE_EXEC_EARLY_EXIT = 1u << 2 /* skip work items whose 3x3 item
-                                     neighbourhood is a flat bed at rest
-                                     (bit-exact: such items are fixed points
-                                     of the step) */
+    SWE_EXEC_EARLY_EXIT = 1u << 2, /* skip work items whose 3x3 item
+                                      neighbourhood is a flat bed at rest
+                                      (bit-exact: such items are fixed points
+                                      of the step) */
+    SWE_EXEC_LOCAL_GROUP = 1u << 3 /* nranks > 1 without NCCL: the ranks are
+                                      contexts of this process on one device,
+                                      driven by one host thread each; nccl_id
+                                      points to SWE_NCCL_ID_BYTES naming the
+                                      group.  Collectives are CUDA-event-ordered
+                                      copies (test transport for the strip
+                                      path on a single GPU; no CUDA graphs) */
 };
 
 typedef struct swe_exec {

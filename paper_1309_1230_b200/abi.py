@@ -25,6 +25,7 @@ SWE_BC_FIXED_ETA = 3
 SWE_EXEC_EXACT = 1 << 0
 SWE_EXEC_NO_GRAPH = 1 << 1
 SWE_EXEC_EARLY_EXIT = 1 << 2
+SWE_EXEC_LOCAL_GROUP = 1 << 3
 
 SWE_NCCL_ID_BYTES = 128
 

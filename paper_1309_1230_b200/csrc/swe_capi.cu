@@ -7,7 +7,11 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <condition_variable>
+#include <map>
+#include <mutex>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -336,6 +340,9 @@ std::vector<std::pair<int, int>> partition_scanlines(int ny, int workers) {
 }  // namespace
 
 // ---------------------------------------------------------------- context
+namespace {
+struct Transport;
+}
 struct swe_ctx {
     swe_grid g{};
     swe_physics ph{};
@@ -373,7 +380,8 @@ struct swe_ctx {
     int occ = 1;
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
     int graph_len = 0;
-    ncclComm_t comm = nullptr;
+    Transport* tr = nullptr;  // row-strip collectives (NCCL or local group); null for one rank
+    unsigned long long* d_xr = nullptr;  // local-group allreduce scratch
     unsigned long long launches = 0;
     swe_timing timing{};
     double tz_x = 0, tz_y = 0;
@@ -465,27 +473,184 @@ int validate(const swe_grid* g, const swe_physics* p, const swe_policy* pol,
     return SWE_OK;
 }
 
+// ---------------------------------------------------------------- strip transport
+// The row-strip protocol needs two collectives: an
+// unsigned-max allreduce of the reduction words (error indices are stored
+// complemented, so max = row-major first offender; non-negative doubles order
+// like their bit patterns) and a send/recv of R halo rows with each strip
+// neighbour.  Between GPUs NCCL carries them over NVLink.  The local group
+// carries them between contexts of one process on one device (one host thread
+// per rank, ordered by CUDA events, no kernel ever waits on another rank's):
+// it lets the GPU tests check the whole strip path bit for bit on one B200.
+struct Transport {
+    virtual ~Transport() = default;
+    virtual int allreduce_max(swe_ctx* c, unsigned long long* d, int n, swe_status* st) = 0;
+    // send_up -> (rank+1).recv_down, send_down -> (rank-1).recv_up, `bytes` each;
+    // null pointers where the neighbour does not exist
+    virtual int sendrecv(swe_ctx* c, const void* send_up, void* recv_up, const void* send_down, void* recv_down,
+                         size_t bytes, swe_status* st) = 0;
+    virtual bool capturable() const = 0;  // may be recorded into a CUDA graph
+};
+
+struct NcclTransport final : Transport {
+    ncclComm_t comm = nullptr;
+    ~NcclTransport() override {
+        if (comm && g_nccl.CommDestroy) g_nccl.CommDestroy(comm);
+    }
+    int allreduce_max(swe_ctx* c, unsigned long long* d, int n, swe_status* st) override;
+    int sendrecv(swe_ctx* c, const void* su, void* ru, const void* sd, void* rd, size_t bytes,
+                 swe_status* st) override;
+    bool capturable() const override { return true; }
+};
+
+constexpr int kMaxLocalRanks = 16;
+struct RedPtrs {
+    const unsigned long long* p[kMaxLocalRanks];
+};
+__global__ void max_reduce_kernel(RedPtrs in, int nranks, int n, unsigned long long* out) {
+    const int k = threadIdx.x;
+    if (k >= n) return;
+    unsigned long long m = 0ull;
+    for (int r = 0; r < nranks; ++r) m = max(m, in.p[r][k]);
+    out[k] = m;
+}
+
+struct LocalGroup {
+    std::mutex m;
+    std::condition_variable cv;
+    int n = 0, arrived = 0, refs = 0;
+    unsigned long long gen = 0;
+    bool broken = false;
+    cudaEvent_t ready[kMaxLocalRanks] = {}, done[kMaxLocalRanks] = {};
+    const void* su[kMaxLocalRanks] = {};
+    const void* sd[kMaxLocalRanks] = {};
+    const unsigned long long* red[kMaxLocalRanks] = {};
+    // all ranks arrive (or a 120 s timeout breaks the group, so a failing
+    // test cannot hang the box)
+    bool barrier() {
+        std::unique_lock<std::mutex> lk(m);
+        if (broken) return false;
+        const unsigned long long g = gen;
+        if (++arrived == n) {
+            arrived = 0;
+            ++gen;
+            cv.notify_all();
+            return true;
+        }
+        if (!cv.wait_for(lk, std::chrono::seconds(120), [&] { return gen != g || broken; })) broken = true;
+        if (broken) {
+            cv.notify_all();
+            return false;
+        }
+        return true;
+    }
+};
+std::mutex g_groups_m;
+std::map<std::string, LocalGroup*> g_groups;
+
+struct LocalTransport final : Transport {
+    LocalGroup* grp = nullptr;
+    std::string key;
+    int rank = 0;
+    ~LocalTransport() override {
+        std::lock_guard<std::mutex> lk(g_groups_m);
+        if (grp && --grp->refs == 0) {
+            for (int r = 0; r < grp->n; ++r) {
+                if (grp->ready[r]) cudaEventDestroy(grp->ready[r]);
+                if (grp->done[r]) cudaEventDestroy(grp->done[r]);
+            }
+            g_groups.erase(key);
+            delete grp;
+        }
+    }
+    int allreduce_max(swe_ctx* c, unsigned long long* d, int n, swe_status* st) override;
+    int sendrecv(swe_ctx* c, const void* su, void* ru, const void* sd, void* rd, size_t bytes,
+                 swe_status* st) override;
+    bool capturable() const override { return false; }
+};
+
 double* row_ptr(swe_ctx* c, int which, int lr) {
     return c->d_buf[which] + static_cast<size_t>(lr + c->R) * 3 * c->pitch;
 }
+
+int NcclTransport::allreduce_max(swe_ctx* c, unsigned long long* d, int n, swe_status* st) {
+    NCCL_TRY(g_nccl.AllReduce(d, d, static_cast<size_t>(n), ncclUint64, ncclMax, comm, c->stream));
+    return SWE_OK;
+}
+
+int NcclTransport::sendrecv(swe_ctx* c, const void* su, void* ru, const void* sd, void* rd, size_t bytes,
+                            swe_status* st) {
+    const int rk = c->ex.rank;
+    NCCL_TRY(g_nccl.GroupStart());
+    if (su) NCCL_TRY(g_nccl.Send(su, bytes, ncclUint8, rk + 1, comm, c->stream));
+    if (ru) NCCL_TRY(g_nccl.Recv(ru, bytes, ncclUint8, rk + 1, comm, c->stream));
+    if (sd) NCCL_TRY(g_nccl.Send(sd, bytes, ncclUint8, rk - 1, comm, c->stream));
+    if (rd) NCCL_TRY(g_nccl.Recv(rd, bytes, ncclUint8, rk - 1, comm, c->stream));
+    NCCL_TRY(g_nccl.GroupEnd());
+    return SWE_OK;
+}
+
+#define GROUP_SYNC()                                                                                   \
+    do {                                                                                               \
+        if (!grp->barrier())                                                                           \
+            return set_status(st, SWE_ERR_RUNTIME, -1, -1, 0.0, "local strip group: a rank timed out"); \
+    } while (0)
+
+// post -> barrier -> read the neighbours' posts -> barrier -> wait for the
+// neighbours' reads before the posted rows may change again
+int LocalTransport::sendrecv(swe_ctx* c, const void* su, void* ru, const void* sd, void* rd, size_t bytes,
+                             swe_status* st) {
+    const int r = rank, n = grp->n;
+    grp->su[r] = su;
+    grp->sd[r] = sd;
+    CUDA_TRY(cudaEventRecord(grp->ready[r], c->stream));
+    GROUP_SYNC();
+    if (ru && r + 1 < n) {
+        CUDA_TRY(cudaStreamWaitEvent(c->stream, grp->ready[r + 1], 0));
+        CUDA_TRY(cudaMemcpyAsync(ru, grp->sd[r + 1], bytes, cudaMemcpyDeviceToDevice, c->stream));
+    }
+    if (rd && r > 0) {
+        CUDA_TRY(cudaStreamWaitEvent(c->stream, grp->ready[r - 1], 0));
+        CUDA_TRY(cudaMemcpyAsync(rd, grp->su[r - 1], bytes, cudaMemcpyDeviceToDevice, c->stream));
+    }
+    CUDA_TRY(cudaEventRecord(grp->done[r], c->stream));
+    GROUP_SYNC();
+    if (r + 1 < n) CUDA_TRY(cudaStreamWaitEvent(c->stream, grp->done[r + 1], 0));
+    if (r > 0) CUDA_TRY(cudaStreamWaitEvent(c->stream, grp->done[r - 1], 0));
+    return SWE_OK;
+}
+
+int LocalTransport::allreduce_max(swe_ctx* c, unsigned long long* d, int n, swe_status* st) {
+    const int r = rank, nr = grp->n;
+    grp->red[r] = d;
+    CUDA_TRY(cudaEventRecord(grp->ready[r], c->stream));
+    GROUP_SYNC();
+    RedPtrs in{};
+    for (int k = 0; k < nr; ++k) {
+        CUDA_TRY(cudaStreamWaitEvent(c->stream, grp->ready[k], 0));
+        in.p[k] = grp->red[k];
+    }
+    max_reduce_kernel<<<1, 32, 0, c->stream>>>(in, nr, n, c->d_xr);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaEventRecord(grp->done[r], c->stream));
+    GROUP_SYNC();
+    for (int k = 0; k < nr; ++k) CUDA_TRY(cudaStreamWaitEvent(c->stream, grp->done[k], 0));
+    CUDA_TRY(cudaMemcpyAsync(d, c->d_xr, static_cast<size_t>(n) * sizeof(unsigned long long),
+                             cudaMemcpyDeviceToDevice, c->stream));
+    return SWE_OK;
+}
+#undef GROUP_SYNC
 
 // Exchange R committed rows with the strip neighbours:
 // own top rows -> rank+1's lower halo, own bottom rows -> rank-1's upper halo.
 int halo_exchange(swe_ctx* c, int which, swe_status* st) {
     if (c->ex.nranks <= 1) return SWE_OK;
-    const size_t cnt = static_cast<size_t>(c->R) * 3 * c->pitch;
+    const size_t bytes = static_cast<size_t>(c->R) * 3 * c->pitch * sizeof(double);
     const int rk = c->ex.rank, nr = c->ex.nranks;
-    NCCL_TRY(g_nccl.GroupStart());
-    if (rk + 1 < nr) {
-        NCCL_TRY(g_nccl.Send(row_ptr(c, which, c->nloc - c->R), cnt, ncclFloat64, rk + 1, c->comm, c->stream));
-        NCCL_TRY(g_nccl.Recv(row_ptr(c, which, c->nloc), cnt, ncclFloat64, rk + 1, c->comm, c->stream));
-    }
-    if (rk > 0) {
-        NCCL_TRY(g_nccl.Send(row_ptr(c, which, 0), cnt, ncclFloat64, rk - 1, c->comm, c->stream));
-        NCCL_TRY(g_nccl.Recv(row_ptr(c, which, -c->R), cnt, ncclFloat64, rk - 1, c->comm, c->stream));
-    }
-    NCCL_TRY(g_nccl.GroupEnd());
-    return SWE_OK;
+    const bool up = rk + 1 < nr, down = rk > 0;
+    return c->tr->sendrecv(c, up ? row_ptr(c, which, c->nloc - c->R) : nullptr,
+                           up ? row_ptr(c, which, c->nloc) : nullptr, down ? row_ptr(c, which, 0) : nullptr,
+                           down ? row_ptr(c, which, -c->R) : nullptr, bytes, st);
 }
 
 // Enqueue one step on the stream (no host sync).  `fwd` = sweep parity,
@@ -497,9 +662,9 @@ int enqueue_step(swe_ctx* c, bool fwd, int cand, swe_status* st) {
     CUDA_TRY(swe_launch_step(c->exact, v, c->ncta, c->stream, c->prm));
     ++c->launches;
     if (c->ex.nranks > 1) {
-        NCCL_TRY(g_nccl.AllReduce(c->d_ctl->red, c->d_ctl->red, RED_N, ncclUint64, ncclMax, c->comm,
-                                  c->stream));
-        int rc = halo_exchange(c, cand, st);
+        int rc = c->tr->allreduce_max(c, c->d_ctl->red, RED_N, st);
+        if (rc) return rc;
+        rc = halo_exchange(c, cand, st);
         if (rc) return rc;
         CUDA_TRY(swe_launch_finalize(c->stream, c->prm));
     }
@@ -526,8 +691,10 @@ int run_scan(swe_ctx* c, int which, unsigned long long out[SCAN_N], swe_status* 
                                                             c->nloc, c->j0, c->ph.g, c->g.dx, c->g.dy,
                                                             c->pol.h_min, c->d_scan);
     CUDA_TRY(cudaGetLastError());
-    if (c->ex.nranks > 1)
-        NCCL_TRY(g_nccl.AllReduce(c->d_scan, c->d_scan, SCAN_N, ncclUint64, ncclMax, c->comm, c->stream));
+    if (c->ex.nranks > 1) {
+        int rc = c->tr->allreduce_max(c, c->d_scan, SCAN_N, st);
+        if (rc) return rc;
+    }
     CUDA_TRY(cudaMemcpyAsync(out, c->d_scan, SCAN_N * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                              c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -741,13 +908,38 @@ EXPORT int swe_cuda_create(const swe_grid* grid, const swe_physics* phys, const 
     CUDA_TRY(cudaMemcpyAsync(c->d_ctl, c->h_ctl, sizeof(SweCtl), cudaMemcpyHostToDevice, c->stream));
 
     if (ex.nranks > 1) {
-        std::string err;
-        if (!g_nccl.load(err)) return set_status(st, SWE_ERR_RUNTIME, -1, -1, 0, "%s", err.c_str());
         if (!exec->nccl_id)
             return set_status(st, SWE_ERR_CONFIG, -1, -1, 0, "exec: nranks > 1 requires nccl_id");
-        ncclUniqueId id;
-        std::memcpy(&id, exec->nccl_id, sizeof id);
-        NCCL_TRY(g_nccl.CommInitRank(&c->comm, ex.nranks, id, ex.rank));
+        CUDA_TRY(cudaMalloc(&c->d_xr, 16 * sizeof(unsigned long long)));
+        if (ex.flags & SWE_EXEC_LOCAL_GROUP) {
+            if (ex.nranks > kMaxLocalRanks)
+                return set_status(st, SWE_ERR_CONFIG, -1, -1, 0, "exec: a local group holds at most %d ranks",
+                                  kMaxLocalRanks);
+            auto* t = new LocalTransport();
+            c->tr = t;
+            t->key.assign(static_cast<const char*>(exec->nccl_id), SWE_NCCL_ID_BYTES);
+            t->rank = ex.rank;
+            std::lock_guard<std::mutex> lk(g_groups_m);
+            LocalGroup*& g = g_groups[t->key];
+            if (!g) {
+                g = new LocalGroup();
+                g->n = ex.nranks;
+            }
+            if (g->n != ex.nranks)
+                return set_status(st, SWE_ERR_CONFIG, -1, -1, 0, "exec: local group size mismatch");
+            ++g->refs;
+            t->grp = g;
+            CUDA_TRY(cudaEventCreateWithFlags(&g->ready[ex.rank], cudaEventDisableTiming));
+            CUDA_TRY(cudaEventCreateWithFlags(&g->done[ex.rank], cudaEventDisableTiming));
+        } else {
+            std::string err;
+            if (!g_nccl.load(err)) return set_status(st, SWE_ERR_RUNTIME, -1, -1, 0, "%s", err.c_str());
+            auto* t = new NcclTransport();
+            c->tr = t;
+            ncclUniqueId id;
+            std::memcpy(&id, exec->nccl_id, sizeof id);
+            NCCL_TRY(g_nccl.CommInitRank(&t->comm, ex.nranks, id, ex.rank));
+        }
     }
 
     // K6 diagnosis thresholds (see swe_step.cuh finalize_step)
@@ -808,7 +1000,8 @@ EXPORT void swe_cuda_destroy(swe_ctx* c) {
     if (!c) return;
     if (c->stream) cudaStreamSynchronize(c->stream);
     destroy_graphs(c);
-    if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
+    delete c->tr;
+    cudaFree(c->d_xr);
     for (auto& b : c->d_buf)
         if (b) cudaFree(b);
     cudaFree(c->d_slope);
@@ -854,22 +1047,18 @@ EXPORT int swe_cuda_load(swe_ctx* c, const double* z, const double* h, const dou
     CUDA_TRY(cudaMemsetAsync(d_zp, 0, static_cast<size_t>(zr) * nx * sizeof(double), c->stream));
     CUDA_TRY(cudaMemcpyAsync(d_zp + static_cast<size_t>(R + 1) * nx, z, static_cast<size_t>(nloc) * rowb,
                              cudaMemcpyHostToDevice, c->stream));
-    if (c->ex.nranks > 1) {
+    if (c->ex.nranks > 1) {  // bed halo rows of the strip neighbours (R + 1 each side)
         const int rk = c->ex.rank, nr = c->ex.nranks, H = R + 1;
-        const size_t cnt = static_cast<size_t>(H) * nx;
-        NCCL_TRY(g_nccl.GroupStart());
-        if (rk + 1 < nr) {
-            NCCL_TRY(g_nccl.Send(d_zp + static_cast<size_t>(R + 1 + nloc - H) * nx, cnt, ncclFloat64, rk + 1,
-                                 c->comm, c->stream));
-            NCCL_TRY(g_nccl.Recv(d_zp + static_cast<size_t>(R + 1 + nloc) * nx, cnt, ncclFloat64, rk + 1, c->comm,
-                                 c->stream));
+        const size_t bytes = static_cast<size_t>(H) * nx * sizeof(double);
+        const bool up = rk + 1 < nr, down = rk > 0;
+        int rc = c->tr->sendrecv(c, up ? d_zp + static_cast<size_t>(R + 1 + nloc - H) * nx : nullptr,
+                                 up ? d_zp + static_cast<size_t>(R + 1 + nloc) * nx : nullptr,
+                                 down ? d_zp + static_cast<size_t>(R + 1) * nx : nullptr, down ? d_zp : nullptr,
+                                 bytes, st);
+        if (rc) {
+            cudaFree(d_zp);
+            return rc;
         }
-        if (rk > 0) {
-            NCCL_TRY(g_nccl.Send(d_zp + static_cast<size_t>(R + 1) * nx, cnt, ncclFloat64, rk - 1, c->comm,
-                                 c->stream));
-            NCCL_TRY(g_nccl.Recv(d_zp, cnt, ncclFloat64, rk - 1, c->comm, c->stream));
-        }
-        NCCL_TRY(g_nccl.GroupEnd());
     }
     // edge z arrays (z_w/z_e for local rows [-R, nloc+R), z_s/z_n per column)
     std::vector<double> zw(nloc + 2 * R, 0.0), ze(nloc + 2 * R, 0.0);
@@ -932,11 +1121,11 @@ EXPORT int swe_cuda_load(swe_ctx* c, const double* z, const double* h, const dou
         }
     }
     if (c->ex.nranks > 1) {
-        unsigned* d = c->d_flags + 1;
-        unsigned v = static_cast<unsigned>(clamp);
-        CUDA_TRY(cudaMemcpyAsync(d, &v, sizeof v, cudaMemcpyHostToDevice, c->stream));
-        NCCL_TRY(g_nccl.AllReduce(d, d, 1, ncclUint32, ncclMax, c->comm, c->stream));
-        CUDA_TRY(cudaMemcpyAsync(&v, d, sizeof v, cudaMemcpyDeviceToHost, c->stream));
+        unsigned long long v = static_cast<unsigned long long>(clamp);
+        CUDA_TRY(cudaMemcpyAsync(c->d_scan, &v, sizeof v, cudaMemcpyHostToDevice, c->stream));
+        int rc = c->tr->allreduce_max(c, c->d_scan, 1, st);
+        if (rc) return rc;
+        CUDA_TRY(cudaMemcpyAsync(&v, c->d_scan, sizeof v, cudaMemcpyDeviceToHost, c->stream));
         CUDA_TRY(cudaStreamSynchronize(c->stream));
         clamp = static_cast<int>(v);
     }
@@ -1160,7 +1349,7 @@ EXPORT int swe_cuda_advance(swe_ctx* c, double t_end, uint64_t step_index0, doub
     std::memset(h.red, 0, sizeof h.red);
     int rc = write_ctl(c, st);
     if (rc) return rc;
-    const bool use_graph = !(c->ex.flags & SWE_EXEC_NO_GRAPH);
+    const bool use_graph = !(c->ex.flags & SWE_EXEC_NO_GRAPH) && (!c->tr || c->tr->capturable());
     const int chunk = 64;
     uint64_t launched = 0;
     unsigned long long committed_before = 0;

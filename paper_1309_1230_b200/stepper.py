@@ -190,6 +190,7 @@ class ExecutorKind:
     rank: int = 0
     nranks: int = 1
     early_exit: bool = False  # skip quiet items on a flat bed (bit-exact; SWE_EXEC_EARLY_EXIT)
+    local_group: bool = False  # strips as contexts of one process on one device (SWE_EXEC_LOCAL_GROUP)
 
     def name(self):
         return ("cuda" + ("" if self.nranks == 1 else f":{self.nranks}") + ("" if self.exact else ":fast")
@@ -212,7 +213,8 @@ class Stepper:
         po = abi.swe_policy(pol.cfl, pol.dt_max, pol.dt_min, pol.h_min)
         b = abi.swe_boundary_set(_bc(bounds.north), _bc(bounds.south), _bc(bounds.east), _bc(bounds.west))
         flags = ((abi.SWE_EXEC_EXACT if kind.exact else 0) | (0 if kind.graph else abi.SWE_EXEC_NO_GRAPH)
-                 | (abi.SWE_EXEC_EARLY_EXIT if kind.early_exit else 0))
+                 | (abi.SWE_EXEC_EARLY_EXIT if kind.early_exit else 0)
+                 | (abi.SWE_EXEC_LOCAL_GROUP if kind.local_group else 0))
         self._id_buf = C.create_string_buffer(nccl_id, abi.SWE_NCCL_ID_BYTES) if nccl_id else None
         ex = abi.swe_exec(kind.device, flags, kind.rank, kind.nranks,
                           C.cast(self._id_buf, C.c_void_p) if self._id_buf is not None else None)

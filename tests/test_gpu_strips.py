@@ -1,0 +1,142 @@
+"""Row-strip decomposition on one B200 through the local-group transport.
+
+The strip path (partition_scanlines bands, per-strip padded buffers with R
+halo rows, no in-kernel finalize, unsigned-max allreduce of the reduction
+words, halo send/recv, finalize kernel, bed-halo exchange at load) is the one
+the NCCL build runs across GPUs; SWE_EXEC_LOCAL_GROUP swaps only the
+transport (CUDA-event-ordered device copies between contexts of this process,
+one host thread per rank), so the kernels and the protocol are checked here
+bit for bit against the single-domain run -- the reference's own contract for
+its decomposed executor (executor.hpp:913-1084: bit-identical to naive).
+"""
+import math
+import os
+import threading
+
+import numpy as np
+import pytest
+
+from golden_cases import bits_equal
+from paper_1309_1230_b200 import scenarios as S
+from paper_1309_1230_b200.stepper import ExecutorKind, FieldSet, GridSpec, InstabilityError, Stepper
+
+pytestmark = pytest.mark.gpu
+
+
+def run_single(sc, exact, steps, early=False, api="advance"):
+    st = Stepper(sc.spec, sc.phys, sc.pol, sc.bounds, ExecutorKind(exact=exact, early_exit=early))
+    st.load(sc.build())
+    out = _drive(st, steps, api)
+    fs = st.state()
+    st.close()
+    return fs, out
+
+
+def _drive(st, steps, api):
+    try:
+        if api == "advance":
+            r = st.advance(1e18, 0, math.nan, steps)
+            return ("ok", r.steps, r.dt_next, r.t_final)
+        dt = st.compute_dt(math.inf)
+        for k in range(steps):
+            dt = st.step(dt, k).dt_next
+        return ("ok", steps, dt, st.time())
+    except InstabilityError as e:
+        return ("instability", e.i, e.j, e.t)
+
+
+def run_strips(sc, nranks, exact, steps, early=False, api="advance"):
+    key = os.urandom(16).hex().encode()
+    full = sc.build()
+    results = [None] * nranks
+    states = [None] * nranks
+    errors = []
+
+    def worker(r):
+        try:
+            kind = ExecutorKind(exact=exact, early_exit=early, rank=r, nranks=nranks, local_group=True,
+                                graph=False)
+            st = Stepper(sc.spec, sc.phys, sc.pol, sc.bounds, kind, nccl_id=key)
+            r0, r1 = st.row_begin, st.row_end
+            st.load_rows(full.z[r0:r1], full.h[r0:r1], full.qx[r0:r1], full.qy[r0:r1], full.t)
+            results[r] = _drive(st, steps, api)
+            shape = (r1 - r0, sc.spec.nx)
+            h, qx, qy = np.empty(shape), np.empty(shape), np.empty(shape)
+            st.state_rows(h, qx, qy)
+            states[r] = (r0, r1, h, qx, qy, st.time())
+            st.close()
+        except Exception as e:  # surfaced by the caller
+            errors.append((r, repr(e)))
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(nranks)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    assert not errors, errors
+    fs = FieldSet(sc.spec, full.z.copy())
+    for r0, r1, h, qx, qy, t in states:
+        fs.h[r0:r1], fs.qx[r0:r1], fs.qy[r0:r1], fs.t = h, qx, qy, t
+    assert all(x == results[0] for x in results), results  # every rank sees the same outcome
+    return fs, results[0]
+
+
+def same(a, b):
+    return bits_equal(a.h, b.h) and bits_equal(a.qx, b.qx) and bits_equal(a.qy, b.qy) and a.t == b.t
+
+
+def _rect_channel():
+    sc = S.gen_channel_flood(200, manning_n=0.0)
+    sc.spec = GridSpec(200, 173, 1.0, 1.0)
+    return sc
+
+
+SCEN = {
+    "dam256": lambda: S.gen_square_dam(256, 1.0, 0.5),                       # R = 1, walls
+    "floodplain256": lambda: S.gen_floodplain(256),                          # R = 2 (smoothing)
+    "channel_rect": _rect_channel,                                           # sloped bed, inflow / fixed eta
+}
+
+
+@pytest.mark.parametrize("nranks", [2, 3, 4])
+@pytest.mark.parametrize("name", sorted(SCEN))
+def test_strips_bit_identical_exact(name, nranks):
+    sc = SCEN[name]()
+    ref, rr = run_single(sc, True, 60)
+    got, rg = run_strips(sc, nranks, True, 60)
+    assert rr == rg
+    assert same(ref, got)
+
+
+@pytest.mark.parametrize("name", sorted(SCEN))
+def test_strips_bit_identical_fast(name):
+    sc = SCEN[name]()
+    ref, rr = run_single(sc, False, 60)
+    got, rg = run_strips(sc, 4, False, 60)
+    assert rr == rg
+    assert same(ref, got)
+
+
+def test_strips_host_step_api():
+    sc = S.gen_floodplain(192)
+    ref, rr = run_single(sc, True, 30, api="step")
+    got, rg = run_strips(sc, 3, True, 30, api="step")
+    assert rr == rg and same(ref, got)
+
+
+def test_strips_with_early_exit():
+    sc = S.gen_floodplain(320)
+    ref, rr = run_single(sc, True, 60)
+    got, rg = run_strips(sc, 2, True, 60, early=True)
+    assert rr == rg and same(ref, got)
+
+
+def test_strips_report_first_offender_like_single_domain():
+    """A thin film without smoothing collapses (SURVEY.md §8(d) C5 note); the
+    strips must raise the same InstabilityError (cell and time) as one domain."""
+    sc = S.gen_square_dam(96, 1.0, 0.01)
+    ref, rr = run_single(sc, True, 200)
+    assert rr[0] == "instability"
+    got, rg = run_strips(sc, 4, True, 200)
+    assert rg == rr
+    assert same(ref, got)  # committed state untouched by the failed step, on every strip
