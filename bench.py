@@ -119,8 +119,13 @@ class ClockSampler:
 
 
 def cpu_baseline_sample(sc, cfg, steps=2):
-    """Time the reference itself (oracle/_ref, decomposed:<cores>) on a bounded sample."""
+    """Time the reference itself (oracle/_ref, decomposed:<cores>) on a bounded sample.
+    Grids above 8192^2 are sampled on the same scenario at 8192^2 (per-cell rate):
+    the reference needs ~192 B/cell of host memory."""
     from oracle import oracle as O
+    if sc.spec.cell_count() > 8192 * 8192:
+        from paper_1309_1230_b200 import scenarios as S
+        sc = S.gen_floodplain(8192) if cfg == "c5" else S.gen_square_dam(8192)
     cores = os.cpu_count() or 1
     if O.ref_available():
         kind = "reference"
@@ -193,7 +198,9 @@ def timed_run(sc, kind, nccl_id, args, dist, local, sampler=None):
     world = kind.nranks
     stp = Stepper(sc.spec, sc.phys, sc.pol, sc.bounds, kind, nccl_id=nccl_id)
     r0, r1 = stp.row_begin, stp.row_end
-    if world == 1:
+    if sc.initial is not None:  # generated on the device (swe_cuda_load_initial), bit-identical to the host build
+        stp.load_initial(sc.initial)
+    elif world == 1:
         stp.load(sc.build())
     else:
         fsr = sc.build_rows(r0, r1)
@@ -322,8 +329,10 @@ def main():
                  "value": total_cells * args.steps / d2, "ms_per_step": d2 / args.steps * 1e3,
                  "roofline_frac": round(bpc * cells_local / (d2 / args.steps) / 1e9 / load_peaks()[0], 4)}
 
+    # e2e moves the whole state through pinned host memory: skipped for the
+    # 32768^2 config (60 GB of pinned buffers)
     e2e = (e2e_run(sc, ExecutorKind(exact=head_exact, device=local, early_exit=early), args.e2e_steps)
-           if world == 1 else None)
+           if world == 1 and spec.cell_count() <= 16384 * 16384 else None)
 
     peak, peak_src = load_peaks()
     achieved = bpc * cells_local / (ms * 1e-3) / 1e9

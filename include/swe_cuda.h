@@ -134,6 +134,18 @@ typedef struct swe_step_result {
     int32_t guard_warnings; /* fixed-elevation ghost clamps this step */
 } swe_step_result;
 
+/* InitialCondition (scenarios.hpp:26-42) restricted to the kinds without
+ * transcendental functions; values of `kind` follow InitialCondition::Kind. */
+enum {
+    SWE_IC_FLAT_POOL = 0,     /* h = depth */
+    SWE_IC_CHANNEL_SLOPE = 2, /* z = slope*dx*(nx-1-i), h = depth - z */
+    SWE_IC_DAM_BREAK = 4      /* h = (i+0.5)*dx < split_x ? h_left : h_right */
+};
+typedef struct swe_initial {
+    int32_t kind;
+    double depth, slope, split_x, h_left, h_right;
+} swe_initial;
+
 /* RunReport subset + resume record (run.hpp:21-66, 101-179) */
 typedef struct swe_run_result {
     uint64_t steps;        /* steps committed by this call */
@@ -177,6 +189,13 @@ void swe_cuda_destroy(swe_ctx* ctx);
  * becomes the run's bed; slopes are computed on the device. */
 int swe_cuda_load(swe_ctx* ctx, const double* z, const double* h, const double* qx,
                   const double* qy, double t, swe_status* st);
+
+/* build_initial_state (scenarios.hpp:95-171) + Stepper::load, generated on
+ * the device for this rank's rows (no host arrays; a 32768^2 state would need
+ * 32 GB of host memory).  Bit-identical to the reference's state; fails with
+ * SWE_ERR_CONFIG for drops/vortex (std::exp) and when the stability guard
+ * rejects the state, like the reference. */
+int swe_cuda_load_initial(swe_ctx* ctx, const swe_initial* ic, double t, swe_status* st);
 
 /* Stepper::state (executor.hpp:783-797): copies this rank's rows out.
  * Any of z/h/qx/qy may be NULL to skip that field. */

@@ -190,6 +190,17 @@ public:
         z_ = fs.z;
     }
 
+    // build_initial_state (scenarios.hpp:95-171) + load, generated on the device
+    // (flat_pool / channel_slope / dam_break; SWE_IC_* kinds)
+    void load_initial(const swe_initial& ic, double t = 0.0) {
+        swe_status st{};
+        if (swe_cuda_load_initial(ctx_, &ic, t, &st) != SWE_OK) throw_status(st);
+        z_.assign(static_cast<std::size_t>(spec_.nx) * spec_.ny, 0.0);
+        const std::size_t off = static_cast<std::size_t>(row_begin_) * spec_.nx;
+        if (swe_cuda_state(ctx_, z_.data() + off, nullptr, nullptr, nullptr, nullptr, &st) != SWE_OK)
+            throw_status(st);
+    }
+
     // executor.hpp:783-797
     FieldSet state() const {
         FieldSet fs(spec_);

@@ -5,7 +5,8 @@ The product path is libswe_cuda.so (paper_1309_1230_b200/lib/), built by
 __graft_entry__.build().  There is no CPU fallback.
 """
 from .stepper import (BoundaryKind, BoundarySet, ConfigError, ExecutorKind, FieldSet, GridSpec,  # noqa: F401
-                      InstabilityError, IoError, PhysicsParams, RunResult, StabilityPolicy, StepCollapseError,
+                      InitialCondition, InstabilityError, IoError, PhysicsParams, RunResult, StabilityPolicy,
+                      StepCollapseError,
                       Stepper, StepResult, partition_scanlines)
 
 __version__ = "0.1.0"

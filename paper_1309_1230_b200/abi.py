@@ -68,6 +68,16 @@ class swe_step_result(C.Structure):
     _fields_ = [("dt_used", C.c_double), ("dt_next", C.c_double), ("guard_warnings", C.c_int32)]
 
 
+SWE_IC_FLAT_POOL = 0
+SWE_IC_CHANNEL_SLOPE = 2
+SWE_IC_DAM_BREAK = 4
+
+
+class swe_initial(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("depth", C.c_double), ("slope", C.c_double), ("split_x", C.c_double),
+                ("h_left", C.c_double), ("h_right", C.c_double)]
+
+
 class swe_run_result(C.Structure):
     _fields_ = [("steps", C.c_uint64), ("step_index", C.c_uint64), ("t_final", C.c_double),
                 ("dt_next", C.c_double), ("guard_warnings", C.c_int32)]
@@ -92,6 +102,7 @@ SIGNATURES = {
                                   C.POINTER(C.c_void_p), ST]),
     "swe_cuda_destroy": (None, [C.c_void_p]),
     "swe_cuda_load": (C.c_int, [C.c_void_p, DP, DP, DP, DP, C.c_double, ST]),
+    "swe_cuda_load_initial": (C.c_int, [C.c_void_p, C.POINTER(swe_initial), C.c_double, ST]),
     "swe_cuda_state": (C.c_int, [C.c_void_p, DP, DP, DP, DP, DP, ST]),
     "swe_cuda_step": (C.c_int, [C.c_void_p, C.c_double, C.c_uint64, C.c_double,
                                 C.POINTER(swe_step_result), ST]),

@@ -200,6 +200,66 @@ __global__ void item_elig_kernel(const unsigned char* flat, int nx, int nloc, in
     }
 }
 
+// Bed edge values for the K1 ghosts: z_w / z_e of own rows (local rows
+// [0, nloc) at offset R), from the compact bed rows zp (row lr at lr + R + 1).
+__global__ void edge_z_kernel(const double* zp, int R, int nx, int nloc, double* zw, double* ze) {
+    for (int lr = blockIdx.x * blockDim.x + threadIdx.x; lr < nloc; lr += gridDim.x * blockDim.x) {
+        const double* row = zp + static_cast<size_t>(lr + R + 1) * nx;
+        zw[lr + R] = row[0];
+        ze[lr + R] = row[nx - 1];
+    }
+}
+
+struct BcSet {
+    SweBC bc[4];  // N, S, E, W
+};
+
+// Fixed-elevation clamp diagnostic (grid.hpp:256-263): any fixed-eta edge
+// cell of this rank whose ghost depth eta - z falls below h_min.
+__global__ void clamp_kernel(const double* zp, int R, int nx, int nloc, int own_s, int own_n, BcSet b,
+                             double h_min, unsigned* flag) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    int hit = 0;
+    if (t < nloc) {
+        const double* row = zp + static_cast<size_t>(t + R + 1) * nx;
+        if (b.bc[SWE_EDGE_W].type == SWE_BC_FIXED_ETA && b.bc[SWE_EDGE_W].eta_out - row[0] < h_min) hit = 1;
+        if (b.bc[SWE_EDGE_E].type == SWE_BC_FIXED_ETA && b.bc[SWE_EDGE_E].eta_out - row[nx - 1] < h_min) hit = 1;
+    }
+    if (t < nx) {
+        if (own_s && b.bc[SWE_EDGE_S].type == SWE_BC_FIXED_ETA &&
+            b.bc[SWE_EDGE_S].eta_out - zp[static_cast<size_t>(R + 1) * nx + t] < h_min)
+            hit = 1;
+        if (own_n && b.bc[SWE_EDGE_N].type == SWE_BC_FIXED_ETA &&
+            b.bc[SWE_EDGE_N].eta_out - zp[static_cast<size_t>(R + nloc) * nx + t] < h_min)
+            hit = 1;
+    }
+    if (hit) atomicOr(flag, 1u);
+}
+
+// build_initial_state (scenarios.hpp:95-171) on the device for the kinds
+// without transcendental functions: flat_pool, channel_slope, dam_break.
+// Same expression trees (the TU is compiled -fmad=false), so the state is
+// bit-identical to the reference's; own rows only (strip-local).
+__global__ void initial_kernel(swe_initial ic, double dx, int nx, int nloc, int P, int R, double* buf, double* zp) {
+    const size_t n = static_cast<size_t>(nloc) * nx;
+    for (size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; k < n;
+         k += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int lr = static_cast<int>(k / nx), i = static_cast<int>(k % nx);
+        double z = 0.0, h = ic.depth;
+        if (ic.kind == SWE_IC_CHANNEL_SLOPE) {
+            z = ic.slope * dx * static_cast<double>(nx - 1 - i);
+            h = ic.depth - z;
+        } else if (ic.kind == SWE_IC_DAM_BREAK) {
+            const double x = (i + 0.5) * dx;
+            h = (x < ic.split_x) ? ic.h_left : ic.h_right;
+        }
+        buf[pidx(P, R, lr, 0, i)] = h;
+        buf[pidx(P, R, lr, 1, i)] = 0.0;
+        buf[pidx(P, R, lr, 2, i)] = 0.0;
+        zp[static_cast<size_t>(lr + R + 1) * nx + i] = z;
+    }
+}
+
 // Scan words (max-combined, like the step reduction).
 enum { SCAN_BAD = 0, SCAN_MINR = 1, SCAN_GUARD = 2, SCAN_N = 4 };
 
@@ -372,7 +432,7 @@ struct swe_ctx {
     bool early = false;
     SweCtl* d_ctl = nullptr;
     SweCtl* h_ctl = nullptr;  // pinned mirror
-    std::vector<double> z_host;  // own rows, for state()
+    double* d_zp = nullptr;  // bed rows [-R-1, nloc+R+1) (compact, nx per row, strip halos): state() z, slopes
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     StepParams prm{};
@@ -894,6 +954,7 @@ EXPORT int swe_cuda_create(const swe_grid* grid, const swe_physics* phys, const 
     CUDA_TRY(cudaMalloc(&c->d_ze, zrows * sizeof(double)));
     CUDA_TRY(cudaMalloc(&c->d_zs, grid->nx * sizeof(double)));
     CUDA_TRY(cudaMalloc(&c->d_zn, grid->nx * sizeof(double)));
+    CUDA_TRY(cudaMalloc(&c->d_zp, static_cast<size_t>(c->nloc + 2 * c->R + 2) * grid->nx * sizeof(double)));
     CUDA_TRY(cudaMemsetAsync(c->d_zw, 0, zrows * sizeof(double), c->stream));
     CUDA_TRY(cudaMemsetAsync(c->d_ze, 0, zrows * sizeof(double), c->stream));
     CUDA_TRY(cudaMemsetAsync(c->d_zs, 0, grid->nx * sizeof(double), c->stream));
@@ -1006,6 +1067,7 @@ EXPORT void swe_cuda_destroy(swe_ctx* c) {
         if (b) cudaFree(b);
     cudaFree(c->d_slope);
     cudaFree(c->d_zw);
+    cudaFree(c->d_zp);
     cudaFree(c->d_ze);
     cudaFree(c->d_zs);
     cudaFree(c->d_zn);
@@ -1024,29 +1086,18 @@ EXPORT void swe_cuda_destroy(swe_ctx* c) {
     delete c;
 }
 
-EXPORT int swe_cuda_load(swe_ctx* c, const double* z, const double* h, const double* qx,
-                         const double* qy, double t, swe_status* st) {
-    if (!c) return set_status(st, SWE_ERR_CONFIG, -1, -1, 0, "null context");
-    CUDA_TRY(cudaSetDevice(c->ex.device));
+namespace {
+
+// Everything Stepper::load derives from the bed and the committed state once
+// both sit on the device (state in buffer 0, own bed rows in d_zp): strip
+// halos of the bed, edge bed values, slopes and flat-bed detection, K1 ghosts,
+// the fixed-elevation clamp diagnostic, the launch geometry, the early-exit
+// tables, and the control block.
+int finish_load(swe_ctx* c, double t, swe_status* st) {
     const int nx = c->g.nx, R = c->R, P = c->pitch, nloc = c->nloc;
     const size_t rowb = static_cast<size_t>(nx) * sizeof(double);
-    // committed state into buffer 0 (padded, row-interleaved)
     c->sel = 0;
-    const double* src[3] = {h, qx, qy};
-    for (int f = 0; f < 3; ++f) {
-        double* dst = c->d_buf[0] + (static_cast<size_t>(R) * 3 + f) * P + R;
-        CUDA_TRY(cudaMemcpy2DAsync(dst, 3 * P * sizeof(double), src[f], rowb, rowb, nloc,
-                                   cudaMemcpyHostToDevice, c->stream));
-    }
-    c->z_host.assign(z, z + static_cast<size_t>(nx) * nloc);
-
-    // bed: z rows [-R-1, nloc+R+1) (compact) with strip halos
-    const int zr = nloc + 2 * R + 2;
-    double* d_zp = nullptr;
-    CUDA_TRY(cudaMalloc(&d_zp, static_cast<size_t>(zr) * nx * sizeof(double)));
-    CUDA_TRY(cudaMemsetAsync(d_zp, 0, static_cast<size_t>(zr) * nx * sizeof(double), c->stream));
-    CUDA_TRY(cudaMemcpyAsync(d_zp + static_cast<size_t>(R + 1) * nx, z, static_cast<size_t>(nloc) * rowb,
-                             cudaMemcpyHostToDevice, c->stream));
+    double* d_zp = c->d_zp;
     if (c->ex.nranks > 1) {  // bed halo rows of the strip neighbours (R + 1 each side)
         const int rk = c->ex.rank, nr = c->ex.nranks, H = R + 1;
         const size_t bytes = static_cast<size_t>(H) * nx * sizeof(double);
@@ -1055,25 +1106,20 @@ EXPORT int swe_cuda_load(swe_ctx* c, const double* z, const double* h, const dou
                                  up ? d_zp + static_cast<size_t>(R + 1 + nloc) * nx : nullptr,
                                  down ? d_zp + static_cast<size_t>(R + 1) * nx : nullptr, down ? d_zp : nullptr,
                                  bytes, st);
-        if (rc) {
-            cudaFree(d_zp);
-            return rc;
-        }
+        if (rc) return rc;
     }
     // edge z arrays (z_w/z_e for local rows [-R, nloc+R), z_s/z_n per column)
-    std::vector<double> zw(nloc + 2 * R, 0.0), ze(nloc + 2 * R, 0.0);
-    for (int lr = 0; lr < nloc; ++lr) {
-        zw[lr + R] = z[static_cast<size_t>(lr) * nx];
-        ze[lr + R] = z[static_cast<size_t>(lr) * nx + nx - 1];
-    }
-    CUDA_TRY(cudaMemcpyAsync(c->d_zw, zw.data(), zw.size() * 8, cudaMemcpyHostToDevice, c->stream));
-    CUDA_TRY(cudaMemcpyAsync(c->d_ze, ze.data(), ze.size() * 8, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(cudaMemsetAsync(c->d_zw, 0, (nloc + 2 * R) * sizeof(double), c->stream));
+    CUDA_TRY(cudaMemsetAsync(c->d_ze, 0, (nloc + 2 * R) * sizeof(double), c->stream));
+    edge_z_kernel<<<std::max(1, std::min((nloc + 255) / 256, 148 * 4)), 256, 0, c->stream>>>(d_zp, R, nx, nloc,
+                                                                                             c->d_zw, c->d_ze);
+    CUDA_TRY(cudaGetLastError());
     if (c->j0 == 0)
-        CUDA_TRY(cudaMemcpyAsync(c->d_zs, z, rowb, cudaMemcpyHostToDevice, c->stream));
-    if (c->j0 + nloc == c->g.ny)
-        CUDA_TRY(cudaMemcpyAsync(c->d_zn, z + static_cast<size_t>(nloc - 1) * nx, rowb, cudaMemcpyHostToDevice,
+        CUDA_TRY(cudaMemcpyAsync(c->d_zs, d_zp + static_cast<size_t>(R + 1) * nx, rowb, cudaMemcpyDeviceToDevice,
                                  c->stream));
-    CUDA_TRY(cudaStreamSynchronize(c->stream));  // zw/ze are stack vectors
+    if (c->j0 + nloc == c->g.ny)
+        CUDA_TRY(cudaMemcpyAsync(c->d_zn, d_zp + static_cast<size_t>(R + nloc) * nx, rowb, cudaMemcpyDeviceToDevice,
+                                 c->stream));
 
     // slopes + flat-bed detection
     if (!c->d_slope) CUDA_TRY(cudaMalloc(&c->d_slope, static_cast<size_t>(nloc + 2 * R) * 2 * P * sizeof(double)));
@@ -1082,11 +1128,20 @@ EXPORT int swe_cuda_load(swe_ctx* c, const double* z, const double* h, const dou
     slopes_kernel<<<148 * 4, 256, 0, c->stream>>>(d_zp, c->d_slope, P, R, nx, nloc, c->j0, c->g.ny,
                                                    2.0 * c->g.dx, 2.0 * c->g.dy, c->d_flags);
     CUDA_TRY(cudaGetLastError());
-    unsigned flag = 0;
-    CUDA_TRY(cudaMemcpyAsync(&flag, c->d_flags, sizeof flag, cudaMemcpyDeviceToHost, c->stream));
+    // fixed-elevation clamp diagnostic (grid.hpp:256-263): depends on the bed only
+    {
+        BcSet b;
+        for (int e = 0; e < 4; ++e) b.bc[e] = c->prm.bc[e];
+        const int n = std::max(nloc, nx);
+        clamp_kernel<<<(n + 255) / 256, 256, 0, c->stream>>>(d_zp, R, nx, nloc, c->j0 == 0, c->j0 + nloc == c->g.ny,
+                                                            b, c->pol.h_min, c->d_flags + 1);
+        CUDA_TRY(cudaGetLastError());
+    }
+    unsigned flags[2] = {0u, 0u};
+    CUDA_TRY(cudaMemcpyAsync(flags, c->d_flags, sizeof flags, cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
-    cudaFree(d_zp);
-    c->flat = (flag == 0);
+    c->flat = (flags[0] == 0);
+    int clamp = flags[1] ? 1 : 0;
     c->prm.slope = c->d_slope;
     {
         std::string err;
@@ -1103,27 +1158,10 @@ EXPORT int swe_cuda_load(swe_ctx* c, const double* z, const double* h, const dou
     int rc = halo_exchange(c, 0, st);
     if (rc) return rc;
 
-    // fixed-elevation clamp diagnostic (grid.hpp:256-263): depends on the bed only
-    int clamp = 0;
-    const swe_boundary* bs[4] = {&c->bnd.north, &c->bnd.south, &c->bnd.east, &c->bnd.west};
-    for (int e = 0; e < 4; ++e) {
-        if (bs[e]->type != SWE_BC_FIXED_ETA) continue;
-        const double eta = bs[e]->eta_out;
-        if (e == SWE_EDGE_W || e == SWE_EDGE_E) {
-            for (int lr = 0; lr < nloc; ++lr) {
-                const double zz = (e == SWE_EDGE_W) ? zw[lr + R] : ze[lr + R];
-                if (eta - zz < c->pol.h_min) clamp = 1;
-            }
-        } else if ((e == SWE_EDGE_S && c->j0 == 0) || (e == SWE_EDGE_N && c->j0 + nloc == c->g.ny)) {
-            const double* zr0 = (e == SWE_EDGE_S) ? z : z + static_cast<size_t>(nloc - 1) * nx;
-            for (int i = 0; i < nx; ++i)
-                if (eta - zr0[i] < c->pol.h_min) clamp = 1;
-        }
-    }
     if (c->ex.nranks > 1) {
         unsigned long long v = static_cast<unsigned long long>(clamp);
         CUDA_TRY(cudaMemcpyAsync(c->d_scan, &v, sizeof v, cudaMemcpyHostToDevice, c->stream));
-        int rc = c->tr->allreduce_max(c, c->d_scan, 1, st);
+        rc = c->tr->allreduce_max(c, c->d_scan, 1, st);
         if (rc) return rc;
         CUDA_TRY(cudaMemcpyAsync(&v, c->d_scan, sizeof v, cudaMemcpyDeviceToHost, c->stream));
         CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -1207,6 +1245,61 @@ EXPORT int swe_cuda_load(swe_ctx* c, const double* z, const double* h, const dou
     return ok_status(st);
 }
 
+}  // namespace
+
+EXPORT int swe_cuda_load(swe_ctx* c, const double* z, const double* h, const double* qx,
+                         const double* qy, double t, swe_status* st) {
+    if (!c) return set_status(st, SWE_ERR_CONFIG, -1, -1, 0, "null context");
+    if (!z || !h || !qx || !qy) return set_status(st, SWE_ERR_CONFIG, -1, -1, 0, "Stepper::load: null field");
+    CUDA_TRY(cudaSetDevice(c->ex.device));
+    c->loaded = false;
+    const int nx = c->g.nx, R = c->R, P = c->pitch, nloc = c->nloc;
+    const size_t rowb = static_cast<size_t>(nx) * sizeof(double);
+    // committed state into buffer 0 (padded, row-interleaved), bed into d_zp
+    const double* src[3] = {h, qx, qy};
+    for (int f = 0; f < 3; ++f) {
+        double* dst = c->d_buf[0] + (static_cast<size_t>(R) * 3 + f) * P + R;
+        CUDA_TRY(cudaMemcpy2DAsync(dst, 3 * P * sizeof(double), src[f], rowb, rowb, nloc,
+                                   cudaMemcpyHostToDevice, c->stream));
+    }
+    CUDA_TRY(cudaMemsetAsync(c->d_zp, 0, static_cast<size_t>(nloc + 2 * R + 2) * rowb, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->d_zp + static_cast<size_t>(R + 1) * nx, z, static_cast<size_t>(nloc) * rowb,
+                             cudaMemcpyHostToDevice, c->stream));
+    return finish_load(c, t, st);
+}
+
+EXPORT int swe_cuda_load_initial(swe_ctx* c, const swe_initial* ic, double t, swe_status* st) {
+    if (!c || !ic) return set_status(st, SWE_ERR_CONFIG, -1, -1, 0, "null context or initial condition");
+    if (ic->kind != SWE_IC_FLAT_POOL && ic->kind != SWE_IC_CHANNEL_SLOPE && ic->kind != SWE_IC_DAM_BREAK)
+        return set_status(st, SWE_ERR_CONFIG, -1, -1, 0,
+                          "load_initial: kind %d is not generated on the device (drops/vortex use std::exp, "
+                          "which is not bit-reproducible on CUDA); load a host FieldSet instead",
+                          ic->kind);
+    CUDA_TRY(cudaSetDevice(c->ex.device));
+    c->loaded = false;
+    const int nx = c->g.nx, R = c->R, nloc = c->nloc;
+    CUDA_TRY(cudaMemsetAsync(c->d_zp, 0, static_cast<size_t>(nloc + 2 * R + 2) * nx * sizeof(double), c->stream));
+    const size_t n = static_cast<size_t>(nloc) * nx;
+    const int blocks = static_cast<int>(std::min<size_t>((n + 255) / 256, 148 * 16));
+    initial_kernel<<<std::max(blocks, 1), 256, 0, c->stream>>>(*ic, c->g.dx, nx, nloc, c->pitch, R, c->d_buf[0],
+                                                               c->d_zp);
+    CUDA_TRY(cudaGetLastError());
+    int rc = finish_load(c, t, st);
+    if (rc) return rc;
+    // build_initial_state ends with the stability guard (scenarios.hpp:165-169)
+    unsigned long long sc[SCAN_N];
+    rc = run_scan(c, 0, sc, st);
+    if (rc) return rc;
+    if (sc[SCAN_GUARD]) {
+        c->loaded = false;
+        const unsigned long long idx = ~sc[SCAN_GUARD];
+        return set_status(st, SWE_ERR_CONFIG, static_cast<int>(idx % nx), static_cast<int>(idx / nx), t,
+                          "initial state fails the stability guard: cell (%d, %d)", static_cast<int>(idx % nx),
+                          static_cast<int>(idx / nx));
+    }
+    return ok_status(st);
+}
+
 EXPORT int swe_cuda_state(swe_ctx* c, double* z, double* h, double* qx, double* qy, double* t,
                           swe_status* st) {
     if (!c || !c->loaded) return set_status(st, SWE_ERR_CONFIG, -1, -1, 0, "Stepper::state: no state loaded");
@@ -1220,8 +1313,10 @@ EXPORT int swe_cuda_state(swe_ctx* c, double* z, double* h, double* qx, double* 
         CUDA_TRY(cudaMemcpy2DAsync(dst[f], rowb, src, 3 * P * sizeof(double), rowb, c->nloc,
                                    cudaMemcpyDeviceToHost, c->stream));
     }
+    if (z)
+        CUDA_TRY(cudaMemcpyAsync(z, c->d_zp + static_cast<size_t>(R + 1) * nx, static_cast<size_t>(c->nloc) * rowb,
+                                 cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
-    if (z) std::memcpy(z, c->z_host.data(), c->z_host.size() * sizeof(double));
     if (t) *t = c->t;
     return ok_status(st);
 }

@@ -11,7 +11,8 @@ import math
 
 import numpy as np
 
-from .stepper import BoundaryKind, BoundarySet, FieldSet, GridSpec, PhysicsParams, StabilityPolicy
+from .stepper import (BoundaryKind, BoundarySet, FieldSet, GridSpec, InitialCondition, PhysicsParams,
+                      StabilityPolicy)
 
 SCENARIO_CFL = 0.45  # scenarios.hpp:177
 
@@ -45,9 +46,10 @@ class Scenario:
     state on a grid; every IC here is uniform along y, so build_rows() can
     materialise one rank's strip without the full grid."""
 
-    def __init__(self, name, spec, phys, pol, bounds, t_end, ic):
+    def __init__(self, name, spec, phys, pol, bounds, t_end, ic, initial=None):
         self.name, self.spec, self.phys, self.pol, self.bounds, self.t_end, self.ic = (
             name, spec, phys, pol, bounds, t_end, ic)
+        self.initial = initial  # InitialCondition for on-device generation (Stepper.load_initial)
 
     def build(self) -> FieldSet:
         return self.ic(self.spec)
@@ -64,7 +66,8 @@ def gen_channel_flood(n: int = 1024, manning_n: float = 0.035) -> Scenario:
     bounds = BoundarySet(north=BoundaryKind.wall(), south=BoundaryKind.wall(),
                          east=BoundaryKind.fixed_eta(1.0), west=BoundaryKind.inflow(0.1, 1.0))
     return Scenario("channel-flood", spec, PhysicsParams(manning_n=manning_n), StabilityPolicy(cfl=SCENARIO_CFL),
-                    bounds, 1000.0, lambda sp: channel_slope(sp, 1.0, slope))
+                    bounds, 1000.0, lambda sp: channel_slope(sp, 1.0, slope),
+                    InitialCondition.channel_slope(1.0, slope))
 
 
 def gen_square_dam(n: int, h_left: float = 1.0, h_right: float = 0.5, nu_art: float = 0.0,
@@ -73,7 +76,8 @@ def gen_square_dam(n: int, h_left: float = 1.0, h_right: float = 0.5, nu_art: fl
     spec = GridSpec(n, n, 1.0, 1.0)
     sx = 0.5 * n * spec.dx if split_x is None else split_x
     return Scenario("square-dam", spec, PhysicsParams(nu_art=nu_art), StabilityPolicy(cfl=SCENARIO_CFL),
-                    BoundarySet.all(BoundaryKind.wall()), 1e18, lambda sp: dam_break(sp, sx, h_left, h_right))
+                    BoundarySet.all(BoundaryKind.wall()), 1e18, lambda sp: dam_break(sp, sx, h_left, h_right),
+                    InitialCondition.dam_break(sx, h_left, h_right))
 
 
 def gen_dam_break(n: int = 400, h_l: float = 1.0, h_r: float = 0.5) -> Scenario:

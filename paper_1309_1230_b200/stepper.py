@@ -164,6 +164,30 @@ class FieldSet:
         return FieldSet(self.spec, self.z.copy(), self.h.copy(), self.qx.copy(), self.qy.copy(), self.t)
 
 
+@dataclass(frozen=True)
+class InitialCondition:
+    """InitialCondition (scenarios.hpp:26-42) for the kinds generated on the device."""
+
+    kind: int = abi.SWE_IC_FLAT_POOL
+    depth: float = 1.0
+    slope: float = 0.0
+    split_x: float = 0.0
+    h_left: float = 1.0
+    h_right: float = 1.0
+
+    @staticmethod
+    def flat_pool(depth):
+        return InitialCondition(abi.SWE_IC_FLAT_POOL, depth)
+
+    @staticmethod
+    def channel_slope(depth, slope):
+        return InitialCondition(abi.SWE_IC_CHANNEL_SLOPE, depth, slope)
+
+    @staticmethod
+    def dam_break(split_x, h_left, h_right):
+        return InitialCondition(abi.SWE_IC_DAM_BREAK, 1.0, 0.0, split_x, h_left, h_right)
+
+
 @dataclass
 class StepResult:
     dt_used: float = 0.0
@@ -259,6 +283,14 @@ class Stepper:
         st = abi.swe_status()
         arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in (z, h, qx, qy)]
         rc = self._lib.swe_cuda_load(self._ctx, *[abi.dptr(a) for a in arrs], float(t), C.byref(st))
+        self._check(rc, st)
+
+    def load_initial(self, ic: InitialCondition, t: float = 0.0):
+        """build_initial_state (scenarios.hpp:95-171) + load, generated on the device."""
+        st = abi.swe_status()
+        c_ic = abi.swe_initial(int(ic.kind), float(ic.depth), float(ic.slope), float(ic.split_x),
+                               float(ic.h_left), float(ic.h_right))
+        rc = self._lib.swe_cuda_load_initial(self._ctx, C.byref(c_ic), float(t), C.byref(st))
         self._check(rc, st)
 
     # executor.hpp:783-797

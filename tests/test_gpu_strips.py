@@ -140,3 +140,61 @@ def test_strips_report_first_offender_like_single_domain():
     got, rg = run_strips(sc, 4, True, 200)
     assert rg == rr
     assert same(ref, got)  # committed state untouched by the failed step, on every strip
+
+
+# ---------------------------------------------------------------- on-device initial conditions
+def _load_both(sc):
+    a = Stepper(sc.spec, sc.phys, sc.pol, sc.bounds, ExecutorKind(exact=True))
+    b = Stepper(sc.spec, sc.phys, sc.pol, sc.bounds, ExecutorKind(exact=True))
+    a.load(sc.build())
+    b.load_initial(sc.initial)
+    return a, b
+
+
+@pytest.mark.parametrize("name", ["dam256", "channel_rect", "floodplain256"])
+def test_load_initial_matches_host_build(name):
+    """swe_cuda_load_initial == build_initial_state + load, bit for bit (z too)."""
+    sc = SCEN[name]()
+    a, b = _load_both(sc)
+    sa, sb = a.state(), b.state()
+    assert same(sa, sb) and bits_equal(sa.z, sb.z)
+    ra = a.advance(1e18, 0, math.nan, 25)
+    rb = b.advance(1e18, 0, math.nan, 25)
+    assert ra.dt_next == rb.dt_next and same(a.state(), b.state())
+
+
+def test_load_initial_rejects_guard_failure_and_exp_kinds():
+    from paper_1309_1230_b200.stepper import ConfigError, InitialCondition
+    sc = S.gen_square_dam(64, 1.0, 0.0)  # h_right below h_min: build_initial_state's guard throws
+    st = Stepper(sc.spec, sc.phys, sc.pol, sc.bounds, ExecutorKind())
+    with pytest.raises(ConfigError):
+        st.load_initial(sc.initial)
+    with pytest.raises(ConfigError):
+        st.load_initial(InitialCondition(kind=1))  # drops: std::exp, host-built only
+
+
+def test_load_initial_on_strips():
+    sc = S.gen_channel_flood(160, manning_n=0.0)
+    ref, rr = run_single(sc, True, 30)
+    key = os.urandom(16).hex().encode()
+    outs, errs = [None] * 3, []
+
+    def worker(r):
+        try:
+            st = Stepper(sc.spec, sc.phys, sc.pol, sc.bounds,
+                         ExecutorKind(rank=r, nranks=3, local_group=True), nccl_id=key)
+            st.load_initial(sc.initial)
+            res = _drive(st, 30, "advance")
+            outs[r] = (st.row_begin, st.row_end, st.state(), res)
+            st.close()
+        except Exception as e:
+            errs.append(repr(e))
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(3)]
+    [t.start() for t in th]
+    [t.join(timeout=600) for t in th]
+    assert not errs, errs
+    for r0, r1, fs, res in outs:
+        assert res == rr
+        assert bits_equal(fs.h[r0:r1], ref.h[r0:r1]) and bits_equal(fs.qx[r0:r1], ref.qx[r0:r1])
+        assert bits_equal(fs.qy[r0:r1], ref.qy[r0:r1]) and bits_equal(fs.z[r0:r1], ref.z[r0:r1])
