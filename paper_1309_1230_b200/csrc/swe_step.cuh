@@ -196,8 +196,9 @@ struct Carry {
     double srx, sry, zx, zy;   // its source term and bed slopes
     CellVec Hyp;               // y face (b-S, b)
     CellVec Uc;                // committed state of the stage-3 row c = b-S
-    double c_srx, c_sry, c_ssx, c_ssy;  // S(U) and S(U*) of row c
-    CellVec c_hs, c_hn, c_hx;  // y faces and own x face of row c
+    double c_sx, c_sy;         // S(U) + S(U*) of row c (summed as the corrector does)
+    CellVec c_dy;              // (dt/dy) * (H_north - H_south) of row c (its y-face term)
+    CellVec c_hx;              // own x face of row c (the other one comes from the neighbour lane)
     CellVec Cp, Cpp;           // corrector output of rows c-S, c-2S (smoothing)
 };
 
@@ -555,7 +556,8 @@ struct Marcher {
 
             const Rc rcS = A::recip(Us.h);
             const Flux FS = A::flux(Us, rcS, half_g);
-            source_of<EXACT, MANNING>(Us, FS, rcS, in.zx, in.zy, neg_g, gnn, out.c_ssx, out.c_ssy);
+            double ssx, ssy;
+            source_of<EXACT, MANNING>(Us, FS, rcS, in.zx, in.zy, neg_g, gnn, ssx, ssy);
 
             // own x face (FWD: east, BWD: west) and y face (b, b+S)   scheme.hpp:153-161
             CellVec Hx = {avg(fn_h, Us.qx), avg(fn_qx, FS.fxx), avg(fn_qy, FS.fxy)};
@@ -571,12 +573,17 @@ struct Marcher {
                     if (gv && i == (FWD ? -1 : p.nx)) Hx = {gh, gqx, gqy};
                 }
             }
-            out.c_hs = FWD ? hy_a : hy_b;
-            out.c_hn = FWD ? hy_b : hy_a;
+            // the corrector's y-face term and source sum are formed here, so row c
+            // carries 8 doubles less into stage 3 (same operations, same order)
+            {
+                const CellVec& hs = FWD ? hy_a : hy_b;
+                const CellVec& hn = FWD ? hy_b : hy_a;
+                out.c_dy = {cy * (hn.h - hs.h), cy * (hn.qx - hs.qx), cy * (hn.qy - hs.qy)};
+            }
             out.c_hx = Hx;
             out.Uc = U;
-            out.c_srx = in.srx;
-            out.c_sry = in.sry;
+            out.c_sx = in.srx + ssx;
+            out.c_sy = in.sry + ssy;
         }
 
         if constexpr (DO3) {
@@ -584,20 +591,22 @@ struct Marcher {
             const CellVec ot = {shf_back(in.c_hx.h), shf_back(in.c_hx.qx), shf_back(in.c_hx.qy)};
             const CellVec hw = FWD ? ot : in.c_hx, he = FWD ? in.c_hx : ot;
             CellVec C;
+            // exact: cx = dt/dx, cy = dt/dy (scheme.hpp:185-191 evaluation order);
+            // fast: faces are plain sums, cx = dt/(2dx), cy = dt/(2dy)
             if constexpr (EXACT) {
-                const double fs_h = dtdx * (he.h - hw.h) + dtdy * (in.c_hn.h - in.c_hs.h);
-                const double fs_qx = dtdx * (he.qx - hw.qx) + dtdy * (in.c_hn.qx - in.c_hs.qx);
-                const double fs_qy = dtdx * (he.qy - hw.qy) + dtdy * (in.c_hn.qy - in.c_hs.qy);
+                const double fs_h = cx * (he.h - hw.h) + in.c_dy.h;
+                const double fs_qx = cx * (he.qx - hw.qx) + in.c_dy.qx;
+                const double fs_qy = cx * (he.qy - hw.qy) + in.c_dy.qy;
                 C.h = (in.Uc.h - fs_h) + 0.0;
-                C.qx = (in.Uc.qx - fs_qx) + half_dt * (in.c_srx + in.c_ssx);
-                C.qy = (in.Uc.qy - fs_qy) + half_dt * (in.c_sry + in.c_ssy);
-            } else {  // faces are plain sums here: cx = dt/(2dx), cy = dt/(2dy)
-                const double fs_h = __fma_rn(cx, he.h - hw.h, cy * (in.c_hn.h - in.c_hs.h));
-                const double fs_qx = __fma_rn(cx, he.qx - hw.qx, cy * (in.c_hn.qx - in.c_hs.qx));
-                const double fs_qy = __fma_rn(cx, he.qy - hw.qy, cy * (in.c_hn.qy - in.c_hs.qy));
+                C.qx = (in.Uc.qx - fs_qx) + half_dt * in.c_sx;
+                C.qy = (in.Uc.qy - fs_qy) + half_dt * in.c_sy;
+            } else {
+                const double fs_h = __fma_rn(cx, he.h - hw.h, in.c_dy.h);
+                const double fs_qx = __fma_rn(cx, he.qx - hw.qx, in.c_dy.qx);
+                const double fs_qy = __fma_rn(cx, he.qy - hw.qy, in.c_dy.qy);
                 C.h = in.Uc.h - fs_h;
-                C.qx = __fma_rn(half_dt, in.c_srx + in.c_ssx, in.Uc.qx - fs_qx);
-                C.qy = __fma_rn(half_dt, in.c_sry + in.c_ssy, in.Uc.qy - fs_qy);
+                C.qx = __fma_rn(half_dt, in.c_sx, in.Uc.qx - fs_qx);
+                C.qy = __fma_rn(half_dt, in.c_sy, in.Uc.qy - fs_qy);
             }
             const int c_row = b - S;
             if constexpr (!SMOOTH) {
