@@ -442,6 +442,12 @@ struct swe_ctx {
     int graph_len = 0;
     Transport* tr = nullptr;  // row-strip collectives (NCCL or local group); null for one rank
     unsigned long long* d_xr = nullptr;  // local-group allreduce scratch
+    // strips: halo exchange overlapped with the interior (edge + interior launches)
+    bool overlap = false;
+    StepParams prm_edge{}, prm_int{};
+    int ncta_edge = 0;
+    cudaStream_t stream_edge = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     unsigned long long launches = 0;
     swe_timing timing{};
     double tz_x = 0, tz_y = 0;
@@ -544,11 +550,11 @@ int validate(const swe_grid* g, const swe_physics* p, const swe_policy* pol,
 // it lets the GPU tests check the whole strip path bit for bit on one B200.
 struct Transport {
     virtual ~Transport() = default;
-    virtual int allreduce_max(swe_ctx* c, unsigned long long* d, int n, swe_status* st) = 0;
+    virtual int allreduce_max(swe_ctx* c, cudaStream_t s, unsigned long long* d, int n, swe_status* st) = 0;
     // send_up -> (rank+1).recv_down, send_down -> (rank-1).recv_up, `bytes` each;
     // null pointers where the neighbour does not exist
-    virtual int sendrecv(swe_ctx* c, const void* send_up, void* recv_up, const void* send_down, void* recv_down,
-                         size_t bytes, swe_status* st) = 0;
+    virtual int sendrecv(swe_ctx* c, cudaStream_t s, const void* send_up, void* recv_up, const void* send_down,
+                         void* recv_down, size_t bytes, swe_status* st) = 0;
     virtual bool capturable() const = 0;  // may be recorded into a CUDA graph
 };
 
@@ -557,8 +563,8 @@ struct NcclTransport final : Transport {
     ~NcclTransport() override {
         if (comm && g_nccl.CommDestroy) g_nccl.CommDestroy(comm);
     }
-    int allreduce_max(swe_ctx* c, unsigned long long* d, int n, swe_status* st) override;
-    int sendrecv(swe_ctx* c, const void* su, void* ru, const void* sd, void* rd, size_t bytes,
+    int allreduce_max(swe_ctx* c, cudaStream_t s, unsigned long long* d, int n, swe_status* st) override;
+    int sendrecv(swe_ctx* c, cudaStream_t s, const void* su, void* ru, const void* sd, void* rd, size_t bytes,
                  swe_status* st) override;
     bool capturable() const override { return true; }
 };
@@ -623,8 +629,8 @@ struct LocalTransport final : Transport {
             delete grp;
         }
     }
-    int allreduce_max(swe_ctx* c, unsigned long long* d, int n, swe_status* st) override;
-    int sendrecv(swe_ctx* c, const void* su, void* ru, const void* sd, void* rd, size_t bytes,
+    int allreduce_max(swe_ctx* c, cudaStream_t s, unsigned long long* d, int n, swe_status* st) override;
+    int sendrecv(swe_ctx* c, cudaStream_t s, const void* su, void* ru, const void* sd, void* rd, size_t bytes,
                  swe_status* st) override;
     bool capturable() const override { return false; }
 };
@@ -633,19 +639,20 @@ double* row_ptr(swe_ctx* c, int which, int lr) {
     return c->d_buf[which] + static_cast<size_t>(lr + c->R) * 3 * c->pitch;
 }
 
-int NcclTransport::allreduce_max(swe_ctx* c, unsigned long long* d, int n, swe_status* st) {
-    NCCL_TRY(g_nccl.AllReduce(d, d, static_cast<size_t>(n), ncclUint64, ncclMax, comm, c->stream));
+int NcclTransport::allreduce_max(swe_ctx* c, cudaStream_t s, unsigned long long* d, int n, swe_status* st) {
+    (void)c;
+    NCCL_TRY(g_nccl.AllReduce(d, d, static_cast<size_t>(n), ncclUint64, ncclMax, comm, s));
     return SWE_OK;
 }
 
-int NcclTransport::sendrecv(swe_ctx* c, const void* su, void* ru, const void* sd, void* rd, size_t bytes,
-                            swe_status* st) {
+int NcclTransport::sendrecv(swe_ctx* c, cudaStream_t s, const void* su, void* ru, const void* sd, void* rd,
+                            size_t bytes, swe_status* st) {
     const int rk = c->ex.rank;
     NCCL_TRY(g_nccl.GroupStart());
-    if (su) NCCL_TRY(g_nccl.Send(su, bytes, ncclUint8, rk + 1, comm, c->stream));
-    if (ru) NCCL_TRY(g_nccl.Recv(ru, bytes, ncclUint8, rk + 1, comm, c->stream));
-    if (sd) NCCL_TRY(g_nccl.Send(sd, bytes, ncclUint8, rk - 1, comm, c->stream));
-    if (rd) NCCL_TRY(g_nccl.Recv(rd, bytes, ncclUint8, rk - 1, comm, c->stream));
+    if (su) NCCL_TRY(g_nccl.Send(su, bytes, ncclUint8, rk + 1, comm, s));
+    if (ru) NCCL_TRY(g_nccl.Recv(ru, bytes, ncclUint8, rk + 1, comm, s));
+    if (sd) NCCL_TRY(g_nccl.Send(sd, bytes, ncclUint8, rk - 1, comm, s));
+    if (rd) NCCL_TRY(g_nccl.Recv(rd, bytes, ncclUint8, rk - 1, comm, s));
     NCCL_TRY(g_nccl.GroupEnd());
     return SWE_OK;
 }
@@ -658,57 +665,58 @@ int NcclTransport::sendrecv(swe_ctx* c, const void* su, void* ru, const void* sd
 
 // post -> barrier -> read the neighbours' posts -> barrier -> wait for the
 // neighbours' reads before the posted rows may change again
-int LocalTransport::sendrecv(swe_ctx* c, const void* su, void* ru, const void* sd, void* rd, size_t bytes,
-                             swe_status* st) {
+int LocalTransport::sendrecv(swe_ctx* c, cudaStream_t s, const void* su, void* ru, const void* sd, void* rd,
+                             size_t bytes, swe_status* st) {
+    (void)c;
     const int r = rank, n = grp->n;
     grp->su[r] = su;
     grp->sd[r] = sd;
-    CUDA_TRY(cudaEventRecord(grp->ready[r], c->stream));
+    CUDA_TRY(cudaEventRecord(grp->ready[r], s));
     GROUP_SYNC();
     if (ru && r + 1 < n) {
-        CUDA_TRY(cudaStreamWaitEvent(c->stream, grp->ready[r + 1], 0));
-        CUDA_TRY(cudaMemcpyAsync(ru, grp->sd[r + 1], bytes, cudaMemcpyDeviceToDevice, c->stream));
+        CUDA_TRY(cudaStreamWaitEvent(s, grp->ready[r + 1], 0));
+        CUDA_TRY(cudaMemcpyAsync(ru, grp->sd[r + 1], bytes, cudaMemcpyDeviceToDevice, s));
     }
     if (rd && r > 0) {
-        CUDA_TRY(cudaStreamWaitEvent(c->stream, grp->ready[r - 1], 0));
-        CUDA_TRY(cudaMemcpyAsync(rd, grp->su[r - 1], bytes, cudaMemcpyDeviceToDevice, c->stream));
+        CUDA_TRY(cudaStreamWaitEvent(s, grp->ready[r - 1], 0));
+        CUDA_TRY(cudaMemcpyAsync(rd, grp->su[r - 1], bytes, cudaMemcpyDeviceToDevice, s));
     }
-    CUDA_TRY(cudaEventRecord(grp->done[r], c->stream));
+    CUDA_TRY(cudaEventRecord(grp->done[r], s));
     GROUP_SYNC();
-    if (r + 1 < n) CUDA_TRY(cudaStreamWaitEvent(c->stream, grp->done[r + 1], 0));
-    if (r > 0) CUDA_TRY(cudaStreamWaitEvent(c->stream, grp->done[r - 1], 0));
+    if (r + 1 < n) CUDA_TRY(cudaStreamWaitEvent(s, grp->done[r + 1], 0));
+    if (r > 0) CUDA_TRY(cudaStreamWaitEvent(s, grp->done[r - 1], 0));
     return SWE_OK;
 }
 
-int LocalTransport::allreduce_max(swe_ctx* c, unsigned long long* d, int n, swe_status* st) {
+int LocalTransport::allreduce_max(swe_ctx* c, cudaStream_t s, unsigned long long* d, int n, swe_status* st) {
     const int r = rank, nr = grp->n;
     grp->red[r] = d;
-    CUDA_TRY(cudaEventRecord(grp->ready[r], c->stream));
+    CUDA_TRY(cudaEventRecord(grp->ready[r], s));
     GROUP_SYNC();
     RedPtrs in{};
     for (int k = 0; k < nr; ++k) {
-        CUDA_TRY(cudaStreamWaitEvent(c->stream, grp->ready[k], 0));
+        CUDA_TRY(cudaStreamWaitEvent(s, grp->ready[k], 0));
         in.p[k] = grp->red[k];
     }
-    max_reduce_kernel<<<1, 32, 0, c->stream>>>(in, nr, n, c->d_xr);
+    max_reduce_kernel<<<1, 32, 0, s>>>(in, nr, n, c->d_xr);
     CUDA_TRY(cudaGetLastError());
-    CUDA_TRY(cudaEventRecord(grp->done[r], c->stream));
+    CUDA_TRY(cudaEventRecord(grp->done[r], s));
     GROUP_SYNC();
-    for (int k = 0; k < nr; ++k) CUDA_TRY(cudaStreamWaitEvent(c->stream, grp->done[k], 0));
+    for (int k = 0; k < nr; ++k) CUDA_TRY(cudaStreamWaitEvent(s, grp->done[k], 0));
     CUDA_TRY(cudaMemcpyAsync(d, c->d_xr, static_cast<size_t>(n) * sizeof(unsigned long long),
-                             cudaMemcpyDeviceToDevice, c->stream));
+                             cudaMemcpyDeviceToDevice, s));
     return SWE_OK;
 }
 #undef GROUP_SYNC
 
 // Exchange R committed rows with the strip neighbours:
 // own top rows -> rank+1's lower halo, own bottom rows -> rank-1's upper halo.
-int halo_exchange(swe_ctx* c, int which, swe_status* st) {
+int halo_exchange(swe_ctx* c, int which, cudaStream_t s, swe_status* st) {
     if (c->ex.nranks <= 1) return SWE_OK;
     const size_t bytes = static_cast<size_t>(c->R) * 3 * c->pitch * sizeof(double);
     const int rk = c->ex.rank, nr = c->ex.nranks;
     const bool up = rk + 1 < nr, down = rk > 0;
-    return c->tr->sendrecv(c, up ? row_ptr(c, which, c->nloc - c->R) : nullptr,
+    return c->tr->sendrecv(c, s, up ? row_ptr(c, which, c->nloc - c->R) : nullptr,
                            up ? row_ptr(c, which, c->nloc) : nullptr, down ? row_ptr(c, which, 0) : nullptr,
                            down ? row_ptr(c, which, -c->R) : nullptr, bytes, st);
 }
@@ -718,13 +726,32 @@ int halo_exchange(swe_ctx* c, int which, swe_status* st) {
 // exchange only).
 int enqueue_step(swe_ctx* c, bool fwd, int cand, swe_status* st) {
     const int v = swe_step_variant(fwd, c->smooth, c->flat, c->manning, c->early);
+    if (c->overlap) {
+        // Strips, overlapped: the edge launch (the bands whose rows the
+        // neighbours need) runs on a high-priority stream and its halo
+        // send/recv follows it there, while the interior launch runs on the
+        // main stream; the allreduce and the finalize wait for both.
+        CUDA_TRY(cudaEventRecord(c->ev_fork, c->stream));
+        CUDA_TRY(cudaStreamWaitEvent(c->stream_edge, c->ev_fork, 0));
+        CUDA_TRY(swe_launch_step(c->exact, v, c->ncta_edge, c->stream_edge, c->prm_edge));
+        int rc = halo_exchange(c, cand, c->stream_edge, st);
+        if (rc) return rc;
+        CUDA_TRY(cudaEventRecord(c->ev_join, c->stream_edge));
+        CUDA_TRY(swe_launch_step(c->exact, v, c->ncta, c->stream, c->prm_int));
+        c->launches += 2;
+        CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+        rc = c->tr->allreduce_max(c, c->stream, c->d_ctl->red, RED_N, st);
+        if (rc) return rc;
+        CUDA_TRY(swe_launch_finalize(c->stream, c->prm));
+        return SWE_OK;
+    }
     if (c->prm.early) CUDA_TRY(swe_launch_schedule(c->exact, c->stream, c->prm));
     CUDA_TRY(swe_launch_step(c->exact, v, c->ncta, c->stream, c->prm));
     ++c->launches;
     if (c->ex.nranks > 1) {
-        int rc = c->tr->allreduce_max(c, c->d_ctl->red, RED_N, st);
+        int rc = c->tr->allreduce_max(c, c->stream, c->d_ctl->red, RED_N, st);
         if (rc) return rc;
-        rc = halo_exchange(c, cand, st);
+        rc = halo_exchange(c, cand, c->stream, st);
         if (rc) return rc;
         CUDA_TRY(swe_launch_finalize(c->stream, c->prm));
     }
@@ -752,7 +779,7 @@ int run_scan(swe_ctx* c, int which, unsigned long long out[SCAN_N], swe_status* 
                                                             c->pol.h_min, c->d_scan);
     CUDA_TRY(cudaGetLastError());
     if (c->ex.nranks > 1) {
-        int rc = c->tr->allreduce_max(c, c->d_scan, SCAN_N, st);
+        int rc = c->tr->allreduce_max(c, c->stream, c->d_scan, SCAN_N, st);
         if (rc) return rc;
     }
     CUDA_TRY(cudaMemcpyAsync(out, c->d_scan, SCAN_N * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
@@ -942,6 +969,13 @@ EXPORT int swe_cuda_create(const swe_grid* grid, const swe_physics* phys, const 
     *out = c;
 
     CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    if (ex.nranks > 1) {
+        int lo = 0, hi = 0;
+        CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        CUDA_TRY(cudaStreamCreateWithPriority(&c->stream_edge, cudaStreamNonBlocking, hi));
+        CUDA_TRY(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+    }
     CUDA_TRY(cudaEventCreate(&c->ev0));
     CUDA_TRY(cudaEventCreate(&c->ev1));
     for (int k = 0; k < 2; ++k) {
@@ -1082,6 +1116,9 @@ EXPORT void swe_cuda_destroy(swe_ctx* c) {
     if (c->h_ctl) cudaFreeHost(c->h_ctl);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
+    if (c->stream_edge) cudaStreamDestroy(c->stream_edge);
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -1102,7 +1139,7 @@ int finish_load(swe_ctx* c, double t, swe_status* st) {
         const int rk = c->ex.rank, nr = c->ex.nranks, H = R + 1;
         const size_t bytes = static_cast<size_t>(H) * nx * sizeof(double);
         const bool up = rk + 1 < nr, down = rk > 0;
-        int rc = c->tr->sendrecv(c, up ? d_zp + static_cast<size_t>(R + 1 + nloc - H) * nx : nullptr,
+        int rc = c->tr->sendrecv(c, c->stream, up ? d_zp + static_cast<size_t>(R + 1 + nloc - H) * nx : nullptr,
                                  up ? d_zp + static_cast<size_t>(R + 1 + nloc) * nx : nullptr,
                                  down ? d_zp + static_cast<size_t>(R + 1) * nx : nullptr, down ? d_zp : nullptr,
                                  bytes, st);
@@ -1155,13 +1192,13 @@ int finish_load(swe_ctx* c, double t, swe_status* st) {
         c->d_buf[0], P, R, nx, nloc, c->j0, c->g.ny, c->prm.bc[SWE_EDGE_W], c->prm.bc[SWE_EDGE_E],
         c->prm.bc[SWE_EDGE_S], c->prm.bc[SWE_EDGE_N], c->d_zw, c->d_ze, c->d_zs, c->d_zn, c->pol.h_min);
     CUDA_TRY(cudaGetLastError());
-    int rc = halo_exchange(c, 0, st);
+    int rc = halo_exchange(c, 0, c->stream, st);
     if (rc) return rc;
 
     if (c->ex.nranks > 1) {
         unsigned long long v = static_cast<unsigned long long>(clamp);
         CUDA_TRY(cudaMemcpyAsync(c->d_scan, &v, sizeof v, cudaMemcpyHostToDevice, c->stream));
-        rc = c->tr->allreduce_max(c, c->d_scan, 1, st);
+        rc = c->tr->allreduce_max(c, c->stream, c->d_scan, 1, st);
         if (rc) return rc;
         CUDA_TRY(cudaMemcpyAsync(&v, c->d_scan, sizeof v, cudaMemcpyDeviceToHost, c->stream));
         CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -1195,6 +1232,10 @@ int finish_load(swe_ctx* c, double t, swe_status* st) {
         c->prm.chunk = static_cast<int>(ch);
         c->prm.nchunks = static_cast<int>((nloc + ch - 1) / ch);
     }
+    c->prm.row_lo = 0;
+    c->prm.row_hi = nloc;
+    c->prm.row_gap = 0;
+    c->prm.wslot = 0;
     destroy_graphs(c);  // variant may have changed
 
     // early-exit tables for this item geometry (flags of both buffers reset:
@@ -1235,6 +1276,24 @@ int finish_load(swe_ctx* c, double t, swe_status* st) {
         c->prm.active = c->d_active;
     }
 
+    // strips: overlap the halo exchange with the interior rows.  The edge
+    // launch covers the kEdge rows at each end of the strip (>= R, the rows the
+    // neighbours receive); the interior launch the rows in between.
+    constexpr int kEdge = 8;
+    c->overlap = c->ex.nranks > 1 && !(c->early && c->flat) && nloc >= 2 * kEdge + 16;
+    if (c->overlap) {
+        c->prm_edge = c->prm;
+        c->prm_edge.chunk = kEdge;
+        c->prm_edge.nchunks = 2;
+        c->prm_edge.row_gap = nloc - 2 * kEdge;
+        c->prm_edge.wslot = 0;
+        c->ncta_edge = std::max(1, std::min(c->ncta, (2 * c->ntiles + SWE_STEP_WPB - 1) / SWE_STEP_WPB));
+        c->prm_int = c->prm;
+        c->prm_int.row_lo = kEdge;
+        c->prm_int.row_hi = nloc - kEdge;
+        c->prm_int.nchunks = (nloc - 2 * kEdge + c->prm.chunk - 1) / c->prm.chunk;
+        c->prm_int.wslot = 1;
+    }
     std::memset(c->h_ctl, 0, sizeof(SweCtl));
     c->h_ctl->t = t;
     c->h_ctl->sel = 0;

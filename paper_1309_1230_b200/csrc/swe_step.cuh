@@ -171,7 +171,8 @@ __device__ __forceinline__ void finalize_step(const StepParams& p, SweCtl* c, do
     }
     for (int k = 0; k < RED_N; ++k) red[k] = 0ull;
     c->finish = 0u;
-    c->work = 0u;
+    c->work[0] = 0u;
+    c->work[1] = 0u;
     c->nactive = 0u;
     __threadfence();
 }
@@ -273,7 +274,7 @@ struct Marcher {
     // built for this step (quiet items already accounted for).
     __device__ __forceinline__ void prod_seg() {
         unsigned item = 0;
-        if (lane == 0) item = atomicAdd(&p.ctl->work, 1u);
+        if (lane == 0) item = atomicAdd(&p.ctl->work[p.wslot], 1u);
         item = __shfl_sync(FULL, item, 0);
         if (item >= nitems) {
             pleft = 0;
@@ -285,8 +286,10 @@ struct Marcher {
         const int tile = static_cast<int>(item % p.ntiles); // windows share halo sectors in L2
         Seg sg;
         sg.tile = tile;
-        sg.ra = rc * p.chunk;
-        sg.rb = min(sg.ra + p.chunk, p.nloc);
+        // rows of this launch: [row_lo, row_hi) in chunks; row_gap jumps from the
+        // first chunk to the second (the strip-edge launch: bottom and top band)
+        sg.ra = p.row_lo + rc * p.chunk + (rc > 0 ? p.row_gap : 0);
+        sg.rb = min(sg.ra + p.chunk, p.row_hi);
         segq[qtail % QN] = sg;
         ++qtail;
         pleft = ((sg.rb - sg.ra) + 2 * R + G - 1) / G;
@@ -802,7 +805,7 @@ __global__ void __launch_bounds__(WPB * 32, SWE_MINB) swe_step_kernel(const __gr
     m.my = 0.0;
     m.e2 = 0;
     m.e4 = m.e5 = 0ull;
-    m.nitems = EARLY ? s_nact : static_cast<unsigned>(p.ntiles) * static_cast<unsigned>(p.nchunks);
+    m.nitems = EARLY ? s_nact : static_cast<unsigned>(p.ntiles) * static_cast<unsigned>(p.nchunks);  // this launch's items
     m.qo = 0ull;
     m.qn = ~0ull;
     m.produce();

@@ -51,7 +51,7 @@ struct __align__(16) SweCtl {
     int err_kind;                 // 2/4/5/6: which plan kernel raised
     int err_i, err_j;
     unsigned int finish;          // CTA arrival counter for the last-block finalize
-    unsigned int work;            // dynamic work-item counter of the step kernel
+    unsigned int work[2];         // dynamic work-item counters (slot per concurrent step launch)
     unsigned int nactive;         // early exit: length of the step's active item list
     unsigned long long red[RED_N];
 };
@@ -87,6 +87,12 @@ struct StepParams {
     int ncta;              // CTAs launched
     int chunk;             // rows per dynamic work item
     int nchunks;           // row chunks per tile (items = ntiles * nchunks)
+    // rows this launch covers: [row_lo, row_hi), chunk rc starting at
+    // row_lo + rc*chunk (+ row_gap for rc > 0); wslot selects the work counter.
+    // One launch per step: [0, nloc), gap 0, slot 0.  Strips with overlap:
+    // an edge launch (the R-deep bands whose rows the neighbours need) and an
+    // interior launch on two streams.
+    int row_lo, row_hi, row_gap, wslot;
     int finalize;          // 1: last CTA finalizes (one rank); 0: host-side allreduce + finalize kernel
     int nranks;
     double dx, dy, g, half_g, neg_g, gnn, h_min, nu;

@@ -50,6 +50,7 @@ def run_strips(sc, nranks, exact, steps, early=False, api="advance"):
     full = sc.build()
     results = [None] * nranks
     states = [None] * nranks
+    launches = [0] * nranks
     errors = []
 
     def worker(r):
@@ -64,6 +65,7 @@ def run_strips(sc, nranks, exact, steps, early=False, api="advance"):
             h, qx, qy = np.empty(shape), np.empty(shape), np.empty(shape)
             st.state_rows(h, qx, qy)
             states[r] = (r0, r1, h, qx, qy, st.time())
+            launches[r] = st.launch_count()
             st.close()
         except Exception as e:  # surfaced by the caller
             errors.append((r, repr(e)))
@@ -78,6 +80,7 @@ def run_strips(sc, nranks, exact, steps, early=False, api="advance"):
     for r0, r1, h, qx, qy, t in states:
         fs.h[r0:r1], fs.qx[r0:r1], fs.qy[r0:r1], fs.t = h, qx, qy, t
     assert all(x == results[0] for x in results), results  # every rank sees the same outcome
+    run_strips.launches = launches
     return fs, results[0]
 
 
@@ -106,6 +109,9 @@ def test_strips_bit_identical_exact(name, nranks):
     got, rg = run_strips(sc, nranks, True, 60)
     assert rr == rg
     assert same(ref, got)
+    # strips of >= 32 rows overlap the halo exchange: an edge and an interior launch per step
+    rows = sc.spec.ny // nranks
+    assert all(n == (2 if rows >= 32 else 1) * 60 for n in run_strips.launches), run_strips.launches
 
 
 @pytest.mark.parametrize("name", sorted(SCEN))
