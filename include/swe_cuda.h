@@ -223,6 +223,14 @@ int swe_cuda_guard(swe_ctx* ctx, swe_status* st);
 int swe_cuda_advance(swe_ctx* ctx, double t_end, uint64_t step_index0, double dt_first,
                      uint64_t max_steps, swe_run_result* res, swe_status* st);
 
+/* swe_cuda_advance that also stops after the first committed step with
+ * t >= t_mark (run_from's snapshot cadence, run.hpp:159-163): the caller
+ * writes the snapshot and calls again with the returned step_index/dt_next.
+ * Stepping decisions are the same as advance's, so the committed states are
+ * identical with or without marks.  t_mark = +inf is swe_cuda_advance. */
+int swe_cuda_advance_marked(swe_ctx* ctx, double t_end, double t_mark, uint64_t step_index0, double dt_first,
+                            uint64_t max_steps, swe_run_result* res, swe_status* st);
+
 /* ---- accessors (executor.hpp:799-805) -------------------------------- */
 double swe_cuda_time(const swe_ctx* ctx);
 int32_t swe_cuda_guard_warnings(const swe_ctx* ctx);

@@ -134,6 +134,7 @@ struct ExecutorKind {
     bool exact = true;  // -fmad=false expression trees: bit-identical to the reference
     bool graph = true;
     bool early_exit = false;  // skip quiet items on a flat bed (bit-exact)
+    bool local_group = false; // strips as contexts of one process on one device (SWE_EXEC_LOCAL_GROUP)
     int rank = 0, nranks = 1;
     const void* nccl_id = nullptr;
     static ExecutorKind cuda(int device = 0, bool exact = true) {
@@ -161,7 +162,7 @@ public:
         swe_exec ex{};
         ex.device = kind.device;
         ex.flags = (kind.exact ? SWE_EXEC_EXACT : 0u) | (kind.graph ? 0u : SWE_EXEC_NO_GRAPH) |
-                   (kind.early_exit ? SWE_EXEC_EARLY_EXIT : 0u);
+                   (kind.early_exit ? SWE_EXEC_EARLY_EXIT : 0u) | (kind.local_group ? SWE_EXEC_LOCAL_GROUP : 0u);
         ex.rank = kind.rank;
         ex.nranks = kind.nranks;
         ex.nccl_id = kind.nccl_id;
@@ -243,6 +244,24 @@ public:
         if (rc != SWE_OK) throw_status(st);
         return last_;
     }
+    // advance() that also stops after the first committed step with t >= t_mark
+    // (run_from's snapshot cadence, run.hpp:159-163)
+    RunResult advance_marked(double t_end, double t_mark, unsigned long long step_index0, double dt_first,
+                             unsigned long long max_steps = 0) {
+        swe_run_result r{};
+        swe_status st{};
+        const int rc = swe_cuda_advance_marked(ctx_, t_end, t_mark, step_index0, dt_first, max_steps, &r, &st);
+        last_ = {r.steps, r.step_index, r.t_final, r.dt_next, r.guard_warnings};
+        if (rc != SWE_OK) throw_status(st);
+        return last_;
+    }
+    // stability_guard (timestep.hpp:112-115) on the committed state
+    void guard() const {
+        swe_status st{};
+        if (swe_cuda_guard(ctx_, &st) != SWE_OK) throw_status(st);
+    }
+    int row_begin() const { return row_begin_; }
+    int row_end() const { return row_end_; }
     const RunResult& last_run() const { return last_; }
     swe_ctx* handle() const { return ctx_; }
 

@@ -83,6 +83,7 @@ def ref_lib():
         L.swr_scenario.argtypes = [C.c_char_p, C.c_int, C.POINTER(abi.swe_grid), C.POINTER(abi.swe_physics),
                                    C.POINTER(abi.swe_policy), C.POINTER(abi.swe_boundary_set), DP, DP, DP, DP,
                                    DP, ST]
+        L.swr_run_config.argtypes = [C.c_char_p, C.c_char_p, C.c_double, ST]
         L.swr_snapshot_bytes.restype = C.c_longlong
         L.swr_snapshot_bytes.argtypes = [C.POINTER(abi.swe_grid), C.c_double, C.c_double, DP, DP, DP, DP,
                                          C.c_char_p, C.c_longlong]
@@ -228,6 +229,12 @@ class RefStepper:
         rc = self.L.swr_guard(self.h, C.byref(st))
         if rc:
             raise_status(st)
+
+
+def ref_run_config(text: str, out_dir: str, snapshot_every: float = -1.0) -> int:
+    """The reference's `run` (parse_config + run, run.hpp:101-179) into out_dir; returns its exit code."""
+    st = abi.swe_status()
+    return ref_lib().swr_run_config(text.encode(), out_dir.encode(), float(snapshot_every), C.byref(st))
 
 
 def ref_scenario(name: str, n: int = 0):

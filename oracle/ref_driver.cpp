@@ -17,6 +17,7 @@
 
 #include "swe/executor.hpp"
 #include "swe/io.hpp"
+#include "swe/run.hpp"
 #include "swe/scenarios.hpp"
 #include "swe/timestep.hpp"
 
@@ -241,4 +242,21 @@ EXPORT long long swr_snapshot_bytes(const swe_grid* g, double t, double gravity,
         std::memcpy(out, bytes.data(), bytes.size());
     }
     return static_cast<long long>(bytes.size());
+}
+
+// The reference's `run` subcommand body (tools/swe_main.cpp cmd_run): parse the
+// config text, integrate to t_end writing SWS1 snapshots and the run report
+// into out_dir (run.hpp:101-179).  The parity target of the C++ CLI.
+EXPORT int swr_run_config(const char* text, const char* out_dir, double snapshot_every, swe_status* st) {
+    try {
+        swe::ScenarioConfig sc = swe::parse_config(text);
+        sc.out_dir = out_dir;
+        if (snapshot_every >= 0.0) sc.snapshot_every = snapshot_every;
+        swe::run(sc, true);
+        if (st) std::memset(st, 0, sizeof *st);
+        return 0;
+    } catch (const std::exception& e) {
+        fill_status(st, code_of(e), &e);
+        return code_of(e);
+    }
 }

@@ -110,6 +110,8 @@ SIGNATURES = {
     "swe_cuda_guard": (C.c_int, [C.c_void_p, ST]),
     "swe_cuda_advance": (C.c_int, [C.c_void_p, C.c_double, C.c_uint64, C.c_double, C.c_uint64,
                                    C.POINTER(swe_run_result), ST]),
+    "swe_cuda_advance_marked": (C.c_int, [C.c_void_p, C.c_double, C.c_double, C.c_uint64, C.c_double, C.c_uint64,
+                                          C.POINTER(swe_run_result), ST]),
     "swe_cuda_time": (C.c_double, [C.c_void_p]),
     "swe_cuda_guard_warnings": (C.c_int32, [C.c_void_p]),
     "swe_cuda_timing": (C.c_int, [C.c_void_p, C.POINTER(swe_timing)]),

@@ -845,7 +845,7 @@ int resolve(swe_ctx* c, swe_status* st) {
         h.step_index += 1;
         h.dt_raw = dt_raw;
         h.steps_done += 1;
-        h.done = (h.mode == 1) ? !(h.t < h.t_end) : 0;
+        h.done = (h.mode == 1) ? (!(h.t < h.t_end) || h.t >= h.t_mark) : 0;
         return write_ctl(c, st);
     }
     if (h.status == SWE_ERR_INSTABILITY) {
@@ -1475,6 +1475,12 @@ EXPORT int swe_cuda_guard(swe_ctx* c, swe_status* st) {
 
 EXPORT int swe_cuda_advance(swe_ctx* c, double t_end, uint64_t step_index0, double dt_first,
                             uint64_t max_steps, swe_run_result* res, swe_status* st) {
+    return swe_cuda_advance_marked(c, t_end, std::numeric_limits<double>::infinity(), step_index0, dt_first,
+                                   max_steps, res, st);
+}
+
+EXPORT int swe_cuda_advance_marked(swe_ctx* c, double t_end, double t_mark, uint64_t step_index0,
+                                   double dt_first, uint64_t max_steps, swe_run_result* res, swe_status* st) {
     if (!c || !c->loaded) return set_status(st, SWE_ERR_CONFIG, -1, -1, 0, "advance: no state loaded");
     if (!is_fin(t_end)) return set_status(st, SWE_ERR_CONFIG, -1, -1, 0, "advance: t_end must be finite");
     CUDA_TRY(cudaSetDevice(c->ex.device));
@@ -1493,11 +1499,12 @@ EXPORT int swe_cuda_advance(swe_ctx* c, double t_end, uint64_t step_index0, doub
     h.mode = 1;
     h.t = c->t;
     h.t_end = t_end;
+    h.t_mark = t_mark;
     h.dt_raw = dt_raw;
     h.step_index = step_index0;
     h.steps_done = 0;
     h.sel = c->sel;
-    h.done = !(c->t < t_end);
+    h.done = !(c->t < t_end) || c->t >= t_mark;
     h.status = 0;
     h.finish = 0;
     std::memset(h.red, 0, sizeof h.red);

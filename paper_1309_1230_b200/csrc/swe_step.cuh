@@ -165,7 +165,7 @@ __device__ __forceinline__ void finalize_step(const StepParams& p, SweCtl* c, do
         c->step_index += 1ull;
         c->dt_raw = dt_next;
         c->steps_done += 1ull;
-        c->done = (c->mode == 1) ? !(tc < c->t_end) : 0;
+        c->done = (c->mode == 1) ? (!(tc < c->t_end) || tc >= c->t_mark) : 0;
     } else {
         c->done = 1;
     }

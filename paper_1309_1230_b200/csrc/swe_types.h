@@ -36,6 +36,7 @@ struct __align__(16) SweCtl {
     double t;                     // committed time
     double dt_raw;                // raw CFL dt for the next step
     double t_end;                 // advance(): landing target
+    double t_mark;                // advance(): also stop once t >= t_mark (snapshot cadence; +inf = off)
     double dt_req;                // step(): dt from the host
     double tcommit_req;           // step(): committed time from the host
     double dt_used, t_commit, dt_next;  // results of the last launch

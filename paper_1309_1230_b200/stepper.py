@@ -350,11 +350,17 @@ class Stepper:
 
     # run.hpp:149-163, device resident
     def advance(self, t_end: float, step_index0: int = 0, dt_first: float = math.nan,
-                max_steps: int = 0) -> RunResult:
+                max_steps: int = 0, t_mark: float = math.inf) -> RunResult:
+        """t_mark: also stop after the first committed step with t >= t_mark
+        (snapshot cadence, run.hpp:159-163; swe_cuda_advance_marked)."""
         res = abi.swe_run_result()
         st = abi.swe_status()
-        rc = self._lib.swe_cuda_advance(self._ctx, float(t_end), int(step_index0), float(dt_first),
-                                        int(max_steps), C.byref(res), C.byref(st))
+        if math.isinf(t_mark):
+            rc = self._lib.swe_cuda_advance(self._ctx, float(t_end), int(step_index0), float(dt_first),
+                                            int(max_steps), C.byref(res), C.byref(st))
+        else:
+            rc = self._lib.swe_cuda_advance_marked(self._ctx, float(t_end), float(t_mark), int(step_index0),
+                                                   float(dt_first), int(max_steps), C.byref(res), C.byref(st))
         self.last_run = RunResult(res.steps, res.step_index, res.t_final, res.dt_next, res.guard_warnings)
         self._check(rc, st)
         return self.last_run
