@@ -253,17 +253,21 @@ def e2e_run(sc, kind, steps):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     st.load_rows(*[p.numpy() for p in pinned], t=0.0)
+    t1 = time.perf_counter()
     dt = st.compute_dt(math.inf)
     for k in range(steps):
         dt = st.step(dt, k).dt_next
+    t2 = time.perf_counter()
     st.state_rows(*[o.numpy() for o in outs])
     el = time.perf_counter() - t0
+    phases = {"load_ms": round((t1 - t0) * 1e3, 2), "steps_ms": round((t2 - t1) * 1e3, 2),
+              "state_ms": round((t0 + el - t2) * 1e3, 2)}
     st.close()
     cells = spec.cell_count()
     ctl = 2 * 200  # control block H2D + D2H per step() call
     return {"value": cells * steps / el, "unit": "cell-steps/s",
             "h2d_bytes_per_step": (4 * cells * 8) // steps + ctl, "d2h_bytes_per_step": (3 * cells * 8) // steps + ctl,
-            "steps": steps, "seconds": el,
+            "steps": steps, "seconds": el, "phases": phases,
             "api": "Stepper.load(host, pinned) + K x Stepper.step() (dt_next read back each step) + "
                    "Stepper.state() (host); C-ABI swe_cuda_load/step/state"}
 

@@ -1125,6 +1125,21 @@ EXPORT void swe_cuda_destroy(swe_ctx* c) {
 
 namespace {
 
+// Guided chunking: the first ~80 % of a launch's rows go out in `chunk`-row
+// items, the rest in quarter-size items, so the dynamic queue ends with short
+// items and the last warps finish together.  SWE_GUIDED=0 keeps uniform chunks.
+void guided_chunks(StepParams& p, int rows) {
+    const char* env = std::getenv("SWE_GUIDED");
+    if (env && env[0] == '0') return;
+    const int c1 = p.chunk, c2 = std::max(8, c1 / 4);
+    if (c1 < 32 || rows < 8 * c1) return;
+    const int big = (rows * 4 / 5) / c1;
+    const int rest = rows - big * c1;
+    p.tier_rc = big;
+    p.chunk2 = c2;
+    p.nchunks = big + (rest + c2 - 1) / c2;
+}
+
 // Everything Stepper::load derives from the bed and the committed state once
 // both sit on the device (state in buffer 0, own bed rows in d_zp): strip
 // halos of the bed, edge bed values, slopes and flat-bed detection, K1 ghosts,
@@ -1236,6 +1251,8 @@ int finish_load(swe_ctx* c, double t, swe_status* st) {
     c->prm.row_hi = nloc;
     c->prm.row_gap = 0;
     c->prm.wslot = 0;
+    c->prm.tier_rc = c->prm.nchunks;  // uniform (the early-exit flags index uniform chunks)
+    c->prm.chunk2 = c->prm.chunk;
     destroy_graphs(c);  // variant may have changed
 
     // early-exit tables for this item geometry (flags of both buffers reset:
@@ -1292,7 +1309,12 @@ int finish_load(swe_ctx* c, double t, swe_status* st) {
         c->prm_int.row_lo = kEdge;
         c->prm_int.row_hi = nloc - kEdge;
         c->prm_int.nchunks = (nloc - 2 * kEdge + c->prm.chunk - 1) / c->prm.chunk;
+        c->prm_int.tier_rc = c->prm_int.nchunks;
         c->prm_int.wslot = 1;
+        c->prm_edge.tier_rc = 2;
+        guided_chunks(c->prm_int, nloc - 2 * kEdge);
+    } else if (!c->prm.early) {
+        guided_chunks(c->prm, nloc);
     }
     std::memset(c->h_ctl, 0, sizeof(SweCtl));
     c->h_ctl->t = t;

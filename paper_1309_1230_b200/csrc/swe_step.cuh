@@ -288,8 +288,14 @@ struct Marcher {
         sg.tile = tile;
         // rows of this launch: [row_lo, row_hi) in chunks; row_gap jumps from the
         // first chunk to the second (the strip-edge launch: bottom and top band)
-        sg.ra = p.row_lo + rc * p.chunk + (rc > 0 ? p.row_gap : 0);
-        sg.rb = min(sg.ra + p.chunk, p.row_hi);
+        // (guided: chunks rc >= tier_rc are chunk2 rows, so the last items are short)
+        if (rc < p.tier_rc) {
+            sg.ra = p.row_lo + rc * p.chunk + (rc > 0 ? p.row_gap : 0);
+            sg.rb = min(sg.ra + p.chunk, p.row_hi);
+        } else {
+            sg.ra = p.row_lo + p.tier_rc * p.chunk + (rc - p.tier_rc) * p.chunk2;
+            sg.rb = min(sg.ra + p.chunk2, p.row_hi);
+        }
         segq[qtail % QN] = sg;
         ++qtail;
         pleft = ((sg.rb - sg.ra) + 2 * R + G - 1) / G;

@@ -94,6 +94,9 @@ struct StepParams {
     // an edge launch (the R-deep bands whose rows the neighbours need) and an
     // interior launch on two streams.
     int row_lo, row_hi, row_gap, wslot;
+    // guided chunking: row chunks rc >= tier_rc hold chunk2 rows (short items
+    // at the end of the dynamic queue trim the tail); tier_rc = nchunks = uniform
+    int tier_rc, chunk2;
     int finalize;          // 1: last CTA finalizes (one rank); 0: host-side allreduce + finalize kernel
     int nranks;
     double dx, dy, g, half_g, neg_g, gnn, h_min, nu;
