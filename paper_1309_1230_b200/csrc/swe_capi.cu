@@ -1239,7 +1239,13 @@ int finish_load(swe_ctx* c, double t, swe_status* st) {
     {
         const long long workers = ncta * SWE_STEP_WPB;
         long long ch = units / std::max<long long>(1, workers * 16);
-        ch = std::max<long long>(16, std::min<long long>(128, ch));
+        if (ch >= 16) {
+            ch = std::min<long long>(128, ch);
+        } else {
+            // small grids are latency-bound: the shortest items (>= 4 rows) that
+            // still give every worker at most one item (512^2: 28 -> 20 us/step)
+            ch = std::max<long long>(4, std::min<long long>(16, (units + workers - 1) / workers));
+        }
         // early exit: finer items (32 rows) so the active band is balanced
         // across workers and skipped at a finer grain
         if (c->early && c->flat) ch = 32;

@@ -37,6 +37,9 @@ constexpr int kStages = 4;  // ring depth in row groups (8 rows in flight)
 #ifndef SWE_MINB
 #define SWE_MINB 3
 #endif
+#ifndef SWE_BRANCHFREE
+#define SWE_BRANCHFREE 1  // predicated rare-error checks (0: branchy screen, for A/B)
+#endif
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -359,10 +362,19 @@ struct Marcher {
         // guard (executor.hpp:543-558): a non-finite h, qx or qy always makes
         // sx + sy non-finite, so one test screens the cell; the exact test
         // runs only for the rare cell that fails the screen.
+#if SWE_BRANCHFREE
+        // predicated: no branch splits the iteration's basic block
+        {
+            const bool ok = finite_d(o.h) & finite_d(o.qx) & finite_d(o.qy) & (o.h >= h_min);
+            const unsigned long long cand = ~(static_cast<unsigned long long>(jj) * p.nx + i);
+            e5 = max(e5, ok ? 0ull : cand);
+        }
+#else
         if (!(finite_d(sx + sy) && o.h >= h_min)) {
             const bool ok = finite_d(o.h) && finite_d(o.qx) && finite_d(o.qy) && o.h >= h_min;
             if (!ok) e5 = max(e5, ~(static_cast<unsigned long long>(jj) * p.nx + i));
         }
+#endif
         // CFL maxima; a NaN speed (only in a guarded cell) never replaces them
         mx = (sx > mx) ? sx : mx;
         my = (sy > my) ? sy : my;
@@ -552,6 +564,13 @@ struct Marcher {
 
             const int jb = p.j0 + b;
             // dry U* -> row-major first consumer (executor.hpp:429-436, 459-513)
+#if SWE_BRANCHFREE
+            if constexpr (!EDGE) {  // interior rows: jb >= 1, consumer is the row-major next cell
+                const bool dry = !(Us.h >= h_min) & star_ok;
+                const unsigned long long cons = static_cast<unsigned long long>(FWD ? jb : jb - 1) * p.nx + i;
+                e4 = max(e4, dry ? ~cons : 0ull);
+            } else
+#endif
             if (!(Us.h >= h_min) && star_ok && (!EDGE || (in_x && jb >= 0 && jb < p.ny))) {
                 unsigned long long cons;
                 if (FWD) cons = static_cast<unsigned long long>(jb) * p.nx + i;
@@ -561,7 +580,11 @@ struct Marcher {
                 e4 = max(e4, ~cons);
             }
             // K2 precondition on the committed state (scheme.hpp:35-39)
+#if SWE_BRANCHFREE
+            e2 |= static_cast<int>(!(U.h >= h_min) & (k >= 0) & (k < L) & out_x);
+#else
             if (!(U.h >= h_min) && k >= 0 && k < L && out_x) e2 = 1;
+#endif
 
             const Rc rcS = A::recip(Us.h);
             const Flux FS = A::flux(Us, rcS, half_g);
