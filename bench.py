@@ -238,19 +238,25 @@ def timed_run(sc, kind, nccl_id, args, dist, local, sampler=None):
     return dev_s, launches, (r1 - r0) * sc.spec.nx
 
 
-def e2e_run(sc, kind, steps):
+def e2e_run(sc, kind, steps, nccl_id=None, dist=None, local=0):
     """The reference-facing API end to end: host FieldSet (pinned) -> load ->
-    K x Stepper.step() (dt_next read back each step) -> state() to host."""
+    K x Stepper.step() (dt_next read back each step) -> state() to host.
+    With N ranks every rank moves its own strip; the time is the max over ranks."""
     import torch
     from paper_1309_1230_b200 import Stepper
     spec = sc.spec
-    pinned = [torch.empty((spec.ny, spec.nx), dtype=torch.float64).pin_memory() for _ in range(4)]
-    src = sc.build()
+    st = Stepper(spec, sc.phys, sc.pol, sc.bounds, kind, nccl_id=nccl_id)
+    r0, r1 = st.row_begin, st.row_end
+    rows = r1 - r0
+    pinned = [torch.empty((rows, spec.nx), dtype=torch.float64).pin_memory() for _ in range(4)]
+    src = sc.build_rows(r0, r1) if kind.nranks > 1 else sc.build()
     for tns, a in zip(pinned, (src.z, src.h, src.qx, src.qy)):
         tns.numpy()[:] = a
-    outs = [torch.empty((spec.ny, spec.nx), dtype=torch.float64).pin_memory() for _ in range(3)]
-    st = Stepper(spec, sc.phys, sc.pol, sc.bounds, kind)
+    del src
+    outs = [torch.empty((rows, spec.nx), dtype=torch.float64).pin_memory() for _ in range(3)]
     torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
     t0 = time.perf_counter()
     st.load_rows(*[p.numpy() for p in pinned], t=0.0)
     t1 = time.perf_counter()
@@ -260,16 +266,21 @@ def e2e_run(sc, kind, steps):
     t2 = time.perf_counter()
     st.state_rows(*[o.numpy() for o in outs])
     el = time.perf_counter() - t0
+    if dist:
+        t = torch.tensor([el], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        el = float(t.item())
     phases = {"load_ms": round((t1 - t0) * 1e3, 2), "steps_ms": round((t2 - t1) * 1e3, 2),
               "state_ms": round((t0 + el - t2) * 1e3, 2)}
     st.close()
     cells = spec.cell_count()
-    ctl = 2 * 200  # control block H2D + D2H per step() call
+    ctl = 2 * 200 * kind.nranks  # control block H2D + D2H per step() call and rank
     return {"value": cells * steps / el, "unit": "cell-steps/s",
             "h2d_bytes_per_step": (4 * cells * 8) // steps + ctl, "d2h_bytes_per_step": (3 * cells * 8) // steps + ctl,
             "steps": steps, "seconds": el, "phases": phases,
             "api": "Stepper.load(host, pinned) + K x Stepper.step() (dt_next read back each step) + "
-                   "Stepper.state() (host); C-ABI swe_cuda_load/step/state"}
+                   "Stepper.state() (host); C-ABI swe_cuda_load/step/state" +
+                   ("; every rank moves its own strip, max over ranks" if kind.nranks > 1 else "")}
 
 
 def main():
@@ -333,10 +344,12 @@ def main():
                  "value": total_cells * args.steps / d2, "ms_per_step": d2 / args.steps * 1e3,
                  "roofline_frac": round(bpc * cells_local / (d2 / args.steps) / 1e9 / load_peaks()[0], 4)}
 
-    # e2e moves the whole state through pinned host memory: skipped for the
-    # 32768^2 config (60 GB of pinned buffers)
-    e2e = (e2e_run(sc, ExecutorKind(exact=head_exact, device=local, early_exit=early), args.e2e_steps)
-           if world == 1 and spec.cell_count() <= 16384 * 16384 else None)
+    # e2e moves the whole state through pinned host memory: skipped when one
+    # rank would hold more than a 16384^2 strip (32768^2 on one GPU: 60 GB pinned)
+    e2e = None
+    if spec.cell_count() // world <= 16384 * 16384:
+        ke = ExecutorKind(exact=head_exact, device=local, rank=rank, nranks=world, early_exit=early)
+        e2e = e2e_run(sc, ke, args.e2e_steps, new_id(), dist, local)
 
     peak, peak_src = load_peaks()
     achieved = bpc * cells_local / (ms * 1e-3) / 1e9

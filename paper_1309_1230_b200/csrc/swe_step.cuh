@@ -34,8 +34,21 @@
 namespace swe_dev {
 
 constexpr int kStages = 4;  // ring depth in row groups (8 rows in flight)
-#ifndef SWE_MINB
-#define SWE_MINB 3
+// Resident CTAs per SM (4 warps each) the register allocation must allow:
+// 4 (16 warps, 128 registers) where the extra warps pay -- exact mode and the
+// flat frictionless step -- and 3 (12 warps, 168 registers) for the fast steps
+// with bathymetry or friction, which run at the board power cap and lose clock
+// with more warps (measured).  SWE_MINB forces one value.
+template <bool EXACT, bool FLAT, bool MANNING>
+constexpr int step_min_blocks() {
+#ifdef SWE_MINB
+    return SWE_MINB;
+#else
+    return (EXACT || (FLAT && !MANNING)) ? 4 : 3;
+#endif
+}
+#ifndef SWE_TWO_STAGE
+#define SWE_TWO_STAGE 1  // corrector in the predictor's iteration (0: one row later, for A/B)
 #endif
 #ifndef SWE_BRANCHFREE
 #define SWE_BRANCHFREE 1  // predicated rare-error checks (0: branchy screen, for A/B)
@@ -620,27 +633,29 @@ struct Marcher {
 
         if constexpr (DO3) {
             // ======== stage 3: corrector of row c = b - S   scheme.hpp:185-191
-            const CellVec ot = {shf_back(in.c_hx.h), shf_back(in.c_hx.qx), shf_back(in.c_hx.qy)};
-            const CellVec hw = FWD ? ot : in.c_hx, he = FWD ? in.c_hx : ot;
+            // (SWE_TWO_STAGE: of row b itself, right after its stage 2)
+            const Carry& cc = SWE_TWO_STAGE ? out : in;
+            const CellVec ot = {shf_back(cc.c_hx.h), shf_back(cc.c_hx.qx), shf_back(cc.c_hx.qy)};
+            const CellVec hw = FWD ? ot : cc.c_hx, he = FWD ? cc.c_hx : ot;
             CellVec C;
             // exact: cx = dt/dx, cy = dt/dy (scheme.hpp:185-191 evaluation order);
             // fast: faces are plain sums, cx = dt/(2dx), cy = dt/(2dy)
             if constexpr (EXACT) {
-                const double fs_h = cx * (he.h - hw.h) + in.c_dy.h;
-                const double fs_qx = cx * (he.qx - hw.qx) + in.c_dy.qx;
-                const double fs_qy = cx * (he.qy - hw.qy) + in.c_dy.qy;
-                C.h = (in.Uc.h - fs_h) + 0.0;
-                C.qx = (in.Uc.qx - fs_qx) + half_dt * in.c_sx;
-                C.qy = (in.Uc.qy - fs_qy) + half_dt * in.c_sy;
+                const double fs_h = cx * (he.h - hw.h) + cc.c_dy.h;
+                const double fs_qx = cx * (he.qx - hw.qx) + cc.c_dy.qx;
+                const double fs_qy = cx * (he.qy - hw.qy) + cc.c_dy.qy;
+                C.h = (cc.Uc.h - fs_h) + 0.0;
+                C.qx = (cc.Uc.qx - fs_qx) + half_dt * cc.c_sx;
+                C.qy = (cc.Uc.qy - fs_qy) + half_dt * cc.c_sy;
             } else {
-                const double fs_h = __fma_rn(cx, he.h - hw.h, in.c_dy.h);
-                const double fs_qx = __fma_rn(cx, he.qx - hw.qx, in.c_dy.qx);
-                const double fs_qy = __fma_rn(cx, he.qy - hw.qy, in.c_dy.qy);
-                C.h = in.Uc.h - fs_h;
-                C.qx = __fma_rn(half_dt, in.c_sx, in.Uc.qx - fs_qx);
-                C.qy = __fma_rn(half_dt, in.c_sy, in.Uc.qy - fs_qy);
+                const double fs_h = __fma_rn(cx, he.h - hw.h, cc.c_dy.h);
+                const double fs_qx = __fma_rn(cx, he.qx - hw.qx, cc.c_dy.qx);
+                const double fs_qy = __fma_rn(cx, he.qy - hw.qy, cc.c_dy.qy);
+                C.h = cc.Uc.h - fs_h;
+                C.qx = __fma_rn(half_dt, cc.c_sx, cc.Uc.qx - fs_qx);
+                C.qy = __fma_rn(half_dt, cc.c_sy, cc.Uc.qy - fs_qy);
             }
-            const int c_row = b - S;
+            const int c_row = SWE_TWO_STAGE ? b : b - S;
             if constexpr (!SMOOTH) {
                 if (EMIT && out_x) emit<EDGE>(C, c_row);
             } else {
@@ -718,6 +733,29 @@ struct Marcher {
         A.Hyp = {0.0, 0.0, 0.0};
         A.Cp = {0.0, 0.0, 0.0};
         A.Cpp = {0.0, 0.0, 0.0};
+#if SWE_TWO_STAGE
+        // corrector of row b in the same iteration as its predictor
+        int k;
+        if constexpr (!SMOOTH) {
+            iter<EDGE, true, false, false, 1>(-1, A, B);  // U* of the halo row
+            k = 0;                                         // 0..L-1: full iterations
+        } else {
+            iter<EDGE, true, false, false, 1>(-2, A, B);  // U* of the outer halo row
+            iter<EDGE, true, true, false, 0>(-1, B, A);   // corrector of the halo row
+            iter<EDGE, true, true, false, 1>(0, A, B);    // first own row: its smoothing waits a row
+            k = 1;                                         // 1..L: smooth + emit row b - S
+        }
+        const int k_last = SMOOTH ? L : L - 1;
+        // carries enter the steady state in B; iterations pair as (B->A GI 0, A->B GI 1)
+        for (; k + 1 <= k_last; k += 2) {
+            iter<EDGE, true, true, true, 0>(k, B, A);
+            iter<EDGE, true, true, true, 1>(k + 1, A, B);
+        }
+        if (k <= k_last) {  // odd steady count: release the half-consumed last group
+            iter<EDGE, true, true, true, 0>(k, B, A);
+            next_group();
+        }
+#else
         int k;
         if constexpr (!SMOOTH) {
             // k = -1, 0: no corrector yet; 1..L-1 steady; L: corrector only
@@ -747,11 +785,12 @@ struct Marcher {
             next_group();  // release the half-consumed last group
             iter<EDGE, false, true, true>(k, A, B);
         }
+#endif
     }
 };
 
 template <int WPB, bool FWD, bool SMOOTH, bool FLAT, bool MANNING, bool EXACT, bool EARLY>
-__global__ void __launch_bounds__(WPB * 32, SWE_MINB) swe_step_kernel(const __grid_constant__ StepParams p) {
+__global__ void __launch_bounds__(WPB * 32, (step_min_blocks<EXACT, FLAT, MANNING>())) swe_step_kernel(const __grid_constant__ StepParams p) {
     using M = Marcher<WPB, FWD, SMOOTH, FLAT, MANNING, EXACT, EARLY>;
     constexpr int D = kStages;
     constexpr int NF = M::NF;
