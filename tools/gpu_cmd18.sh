@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+bash tools/full_bench.sh
+bash tools/ncu_full.sh c3 fast c3_fast
+bash tools/ncu_full.sh c3f exact c3f_exact
