@@ -262,6 +262,10 @@ struct Marcher {
     double mx, my;
     int e2;
     unsigned long long e4, e5;
+    // per-segment row-only error words (this lane's column is fixed within a
+    // segment): ~row of the first offending row, 0 = none; folded into e4/e5
+    // (as ~(row*nx + i)) at the end of the segment
+    unsigned e4r, e5r;
     // quiet-item tracking of the current segment (early exit): with
     // mom = bits(qx) | bits(qy) per output cell, qo |= bits(h) | mom and
     // qn &= bits(h) & ~mom end equal iff every cell is (H, +0, +0), same H
@@ -379,8 +383,7 @@ struct Marcher {
         // predicated: no branch splits the iteration's basic block
         {
             const bool ok = finite_d(o.h) & finite_d(o.qx) & finite_d(o.qy) & (o.h >= h_min);
-            const unsigned long long cand = ~(static_cast<unsigned long long>(jj) * p.nx + i);
-            e5 = max(e5, ok ? 0ull : cand);
+            e5r = max(e5r, ok ? 0u : ~static_cast<unsigned>(jj));
         }
 #else
         if (!(finite_d(sx + sy) && o.h >= h_min)) {
@@ -580,8 +583,7 @@ struct Marcher {
 #if SWE_BRANCHFREE
             if constexpr (!EDGE) {  // interior rows: jb >= 1, consumer is the row-major next cell
                 const bool dry = !(Us.h >= h_min) & star_ok;
-                const unsigned long long cons = static_cast<unsigned long long>(FWD ? jb : jb - 1) * p.nx + i;
-                e4 = max(e4, dry ? ~cons : 0ull);
+                e4r = max(e4r, dry ? ~static_cast<unsigned>(FWD ? jb : jb - 1) : 0u);
             } else
 #endif
             if (!(Us.h >= h_min) && star_ok && (!EDGE || (in_x && jb >= 0 && jb < p.ny))) {
@@ -705,9 +707,12 @@ struct Marcher {
         orow = nxt + static_cast<size_t>(r_start + R) * 3 * P + (i + R);  // first output row
         qo = 0ull;
         qn = ~0ull;
+        e4r = e5r = 0u;
         const int jlo = p.j0 + sg.ra - R - 1, jhi = p.j0 + sg.rb + R;  // rows the march touches, padded
         if (xedge || jlo <= 0 || jhi >= p.ny - 1) march<true>();
         else march<false>();
+        if (e4r) e4 = max(e4, ~(static_cast<unsigned long long>(~e4r) * p.nx + i));
+        if (e5r) e5 = max(e5, ~(static_cast<unsigned long long>(~e5r) * p.nx + i));
         if constexpr (EARLY) {
             // quiet flag of this item in the candidate buffer: the depth bits
             // H when every output cell is (H, +0, +0) with H >= h_min, else 0
