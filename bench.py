@@ -293,7 +293,9 @@ def main():
     ap.add_argument("--fast", action="store_true", help="headline in FAST mode only (skip the exact-mode line)")
     ap.add_argument("--exact", action="store_true", help="headline in EXACT (-fmad=false, bit-identical) mode")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=50)
+    ap.add_argument("--e2e-steps", type=int, default=1000,
+                    help="steps of the end-to-end run (load from host, K x step(), state to host); "
+                         "1000 = the reference run length of config C1")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
