@@ -47,12 +47,6 @@ constexpr int step_min_blocks() {
     return (EXACT || (FLAT && !MANNING)) ? 4 : 3;
 #endif
 }
-#ifndef SWE_TWO_STAGE
-#define SWE_TWO_STAGE 1  // corrector in the predictor's iteration (0: one row later, for A/B)
-#endif
-#ifndef SWE_BRANCHFREE
-#define SWE_BRANCHFREE 1  // predicated rare-error checks (0: branchy screen, for A/B)
-#endif
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -195,28 +189,33 @@ __device__ __forceinline__ void finalize_step(const StepParams& p, SweCtl* c, do
 
 // --------------------------------------------------------------- the kernel
 // One warp = one worker.  Lane t owns column i = x0 - R + t of a 32-column
-// window; lanes R..31-R are output columns.  Iteration k of the row march is
-// a 3-stage software pipeline over consecutive rows (march direction S):
+// window; lanes R..31-R are output columns.  Iteration k of the row march
+// works on two consecutive rows (march direction S):
 //   stage 1  row b+S : committed row from the warp's TMA ring; F/G/S(U)
 //   stage 2  row b   : predictor U*, F/G/S(U*), interface fluxes, boundary
-//                      faces, dry-U* detection
-//   stage 3  row b-S : corrector (+ smoothing of row b-2S), guard, CFL, store
-// The three dependency chains interleave within the warp; x neighbours are
-// exchanged with shuffles, so warps never wait for each other.  The steady
-// state is unrolled by two with the pipeline registers ping-ponging between
-// two carry sets, so no register moves are needed to advance the march.
+//                      faces, dry-U* detection -- then, once the neighbour
+//                      lane's x face is shuffled in, the corrector of row b
+//                      (+ smoothing of row b-S), guard, CFL, store
+// Stage 1 of the next row is independent of row b's stage 2, so the two
+// dependency chains interleave; x neighbours are exchanged with shuffles, so
+// warps never wait for each other.  (Running the corrector one iteration
+// later, as a third stage, gave more overlap but carried 11 more doubles per
+// lane and spilled: the two-stage march is 5 % faster.)  The steady state is
+// unrolled by two with the pipeline registers ping-ponging between two carry
+// sets, so no register moves are needed to advance the march.
 
-// Pipeline registers entering an iteration.
+// Pipeline registers between iterations (the c_* members hand row b's stage-2
+// results to its corrector within the same iteration).
 struct Carry {
     CellVec U;                 // committed state of the stage-2 row b
     Flux FU;                   // its fluxes
     double srx, sry, zx, zy;   // its source term and bed slopes
     CellVec Hyp;               // y face (b-S, b)
-    CellVec Uc;                // committed state of the stage-3 row c = b-S
-    double c_sx, c_sy;         // S(U) + S(U*) of row c (summed as the corrector does)
-    CellVec c_dy;              // (dt/dy) * (H_north - H_south) of row c (its y-face term)
-    CellVec c_hx;              // own x face of row c (the other one comes from the neighbour lane)
-    CellVec Cp, Cpp;           // corrector output of rows c-S, c-2S (smoothing)
+    CellVec Uc;                // committed state of the corrector row
+    double c_sx, c_sy;         // S(U) + S(U*) of that row (summed as the corrector does)
+    CellVec c_dy;              // (dt/dy) * (H_north - H_south) of that row (its y-face term)
+    CellVec c_hx;              // its own x face (the other one comes from the neighbour lane)
+    CellVec Cp, Cpp;           // corrector output of rows b-S, b-2S (smoothing)
 };
 
 struct WarpRing {  // per-warp TMA ring state (warp-uniform)
@@ -379,18 +378,11 @@ struct Marcher {
         // guard (executor.hpp:543-558): a non-finite h, qx or qy always makes
         // sx + sy non-finite, so one test screens the cell; the exact test
         // runs only for the rare cell that fails the screen.
-#if SWE_BRANCHFREE
         // predicated: no branch splits the iteration's basic block
         {
             const bool ok = finite_d(o.h) & finite_d(o.qx) & finite_d(o.qy) & (o.h >= h_min);
             e5r = max(e5r, ok ? 0u : ~static_cast<unsigned>(jj));
         }
-#else
-        if (!(finite_d(sx + sy) && o.h >= h_min)) {
-            const bool ok = finite_d(o.h) && finite_d(o.qx) && finite_d(o.qy) && o.h >= h_min;
-            if (!ok) e5 = max(e5, ~(static_cast<unsigned long long>(jj) * p.nx + i));
-        }
-#endif
         // CFL maxima; a NaN speed (only in a guarded cell) never replaces them
         mx = (sx > mx) ? sx : mx;
         my = (sy > my) ? sy : my;
@@ -580,13 +572,10 @@ struct Marcher {
 
             const int jb = p.j0 + b;
             // dry U* -> row-major first consumer (executor.hpp:429-436, 459-513)
-#if SWE_BRANCHFREE
             if constexpr (!EDGE) {  // interior rows: jb >= 1, consumer is the row-major next cell
                 const bool dry = !(Us.h >= h_min) & star_ok;
                 e4r = max(e4r, dry ? ~static_cast<unsigned>(FWD ? jb : jb - 1) : 0u);
-            } else
-#endif
-            if (!(Us.h >= h_min) && star_ok && (!EDGE || (in_x && jb >= 0 && jb < p.ny))) {
+            } else if (!(Us.h >= h_min) && star_ok && (!EDGE || (in_x && jb >= 0 && jb < p.ny))) {
                 unsigned long long cons;
                 if (FWD) cons = static_cast<unsigned long long>(jb) * p.nx + i;
                 else if (jb >= 1) cons = static_cast<unsigned long long>(jb - 1) * p.nx + i;
@@ -595,11 +584,7 @@ struct Marcher {
                 e4 = max(e4, ~cons);
             }
             // K2 precondition on the committed state (scheme.hpp:35-39)
-#if SWE_BRANCHFREE
             e2 |= static_cast<int>(!(U.h >= h_min) & (k >= 0) & (k < L) & out_x);
-#else
-            if (!(U.h >= h_min) && k >= 0 && k < L && out_x) e2 = 1;
-#endif
 
             const Rc rcS = A::recip(Us.h);
             const Flux FS = A::flux(Us, rcS, half_g);
@@ -634,9 +619,8 @@ struct Marcher {
         }
 
         if constexpr (DO3) {
-            // ======== stage 3: corrector of row c = b - S   scheme.hpp:185-191
-            // (SWE_TWO_STAGE: of row b itself, right after its stage 2)
-            const Carry& cc = SWE_TWO_STAGE ? out : in;
+            // ======== stage 3: corrector of row b   scheme.hpp:185-191
+            const Carry& cc = out;  // row b's own stage-2 results (two-stage march)
             const CellVec ot = {shf_back(cc.c_hx.h), shf_back(cc.c_hx.qx), shf_back(cc.c_hx.qy)};
             const CellVec hw = FWD ? ot : cc.c_hx, he = FWD ? cc.c_hx : ot;
             CellVec C;
@@ -657,7 +641,7 @@ struct Marcher {
                 C.qx = __fma_rn(half_dt, cc.c_sx, cc.Uc.qx - fs_qx);
                 C.qy = __fma_rn(half_dt, cc.c_sy, cc.Uc.qy - fs_qy);
             }
-            const int c_row = SWE_TWO_STAGE ? b : b - S;
+            const int c_row = b;
             if constexpr (!SMOOTH) {
                 if (EMIT && out_x) emit<EDGE>(C, c_row);
             } else {
@@ -738,7 +722,6 @@ struct Marcher {
         A.Hyp = {0.0, 0.0, 0.0};
         A.Cp = {0.0, 0.0, 0.0};
         A.Cpp = {0.0, 0.0, 0.0};
-#if SWE_TWO_STAGE
         // corrector of row b in the same iteration as its predictor
         int k;
         if constexpr (!SMOOTH) {
@@ -760,37 +743,6 @@ struct Marcher {
             iter<EDGE, true, true, true, 0>(k, B, A);
             next_group();
         }
-#else
-        int k;
-        if constexpr (!SMOOTH) {
-            // k = -1, 0: no corrector yet; 1..L-1 steady; L: corrector only
-            iter<EDGE, true, false, false, 1>(-1, A, B);
-            iter<EDGE, true, false, false, 0>(0, B, A);
-            k = 1;
-        } else {
-            // k = -2, -1: no corrector; 0, 1: corrector without output;
-            // 2..L steady; L+1: corrector + smoothing only
-            iter<EDGE, true, false, false, 1>(-2, A, B);
-            iter<EDGE, true, false, false, 0>(-1, B, A);
-            iter<EDGE, true, true, false, 1>(0, A, B);
-            iter<EDGE, true, true, false, 0>(1, B, A);
-            k = 2;
-        }
-        const int k_last = SMOOTH ? L : L - 1;  // last steady iteration
-        // march rows consumed so far: 1 + 2R (odd), so steady pairs consume
-        // group rows (1, 0) and an odd tail row 1
-        for (; k + 1 <= k_last; k += 2) {
-            iter<EDGE, true, true, true, 1>(k, A, B);
-            iter<EDGE, true, true, true, 0>(k + 1, B, A);
-        }
-        if (k <= k_last) {  // odd steady count
-            iter<EDGE, true, true, true, 1>(k, A, B);
-            iter<EDGE, false, true, true>(k + 1, B, A);
-        } else {
-            next_group();  // release the half-consumed last group
-            iter<EDGE, false, true, true>(k, A, B);
-        }
-#endif
     }
 };
 
