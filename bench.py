@@ -378,7 +378,7 @@ def main():
     cpu = None
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_baseline_sample(sc, args.config, steps=2)
+            cpu = cpu_baseline_sample(sc, args.config, steps=10)
         except Exception as e:  # the baseline must never kill the GPU bench
             cpu = {"value": None, "error": str(e)}
 

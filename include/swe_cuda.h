@@ -256,7 +256,9 @@ int swe_cuda_selftest_div(const double* a, const double* b, size_t n, int exact,
 
 /* ---- misc ------------------------------------------------------------ */
 const char* swe_cuda_version(void);
-/* Number of step-kernel launches issued since create (bench evidence). */
+/* Number of this library's kernel launches issued for steps since create:
+ * step kernels plus, where used, the early-exit schedule kernel and the strip
+ * finalize kernel (bench evidence). */
 uint64_t swe_cuda_launch_count(const swe_ctx* ctx);
 
 #ifdef __cplusplus

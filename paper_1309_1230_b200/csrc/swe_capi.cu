@@ -440,6 +440,7 @@ struct swe_ctx {
     int occ = 1;
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
     int graph_len = 0;
+    unsigned long long graph_kernels = 0;  // our kernels in one captured graph
     Transport* tr = nullptr;  // row-strip collectives (NCCL or local group); null for one rank
     unsigned long long* d_xr = nullptr;  // local-group allreduce scratch
     // strips: halo exchange overlapped with the interior (edge + interior launches)
@@ -738,14 +739,17 @@ int enqueue_step(swe_ctx* c, bool fwd, int cand, swe_status* st) {
         if (rc) return rc;
         CUDA_TRY(cudaEventRecord(c->ev_join, c->stream_edge));
         CUDA_TRY(swe_launch_step(c->exact, v, c->ncta, c->stream, c->prm_int));
-        c->launches += 2;
         CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
         rc = c->tr->allreduce_max(c, c->stream, c->d_ctl->red, RED_N, st);
         if (rc) return rc;
         CUDA_TRY(swe_launch_finalize(c->stream, c->prm));
+        c->launches += 3 + (c->tr->capturable() ? 0 : 1);  // edge + interior + finalize (+ local max kernel)
         return SWE_OK;
     }
-    if (c->prm.early) CUDA_TRY(swe_launch_schedule(c->exact, c->stream, c->prm));
+    if (c->prm.early) {
+        CUDA_TRY(swe_launch_schedule(c->exact, c->stream, c->prm));
+        ++c->launches;
+    }
     CUDA_TRY(swe_launch_step(c->exact, v, c->ncta, c->stream, c->prm));
     ++c->launches;
     if (c->ex.nranks > 1) {
@@ -754,6 +758,7 @@ int enqueue_step(swe_ctx* c, bool fwd, int cand, swe_status* st) {
         rc = halo_exchange(c, cand, c->stream, st);
         if (rc) return rc;
         CUDA_TRY(swe_launch_finalize(c->stream, c->prm));
+        c->launches += 1 + (c->tr->capturable() ? 0 : 1);  // finalize (+ local max kernel)
     }
     return SWE_OK;
 }
@@ -888,6 +893,7 @@ int destroy_graphs(swe_ctx* c) {
 
 int build_graphs(swe_ctx* c, int len, swe_status* st) {
     destroy_graphs(c);
+    const unsigned long long before = c->launches;
     for (int start = 0; start < 2; ++start) {  // start 0: first launch forward
         cudaGraph_t gph;
         CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
@@ -902,7 +908,8 @@ int build_graphs(swe_ctx* c, int len, swe_status* st) {
         CUDA_TRY(cudaGraphInstantiate(&c->graph[start], gph, 0));
         cudaGraphDestroy(gph);
     }
-    c->launches -= static_cast<unsigned long long>(2 * len);  // captured, not launched
+    c->graph_kernels = (c->launches - before) / 2;  // our kernels per graph launch
+    c->launches = before;                          // captured, not launched
     c->graph_len = len;
     return SWE_OK;
 }
@@ -1565,7 +1572,7 @@ EXPORT int swe_cuda_advance_marked(swe_ctx* c, double t_end, double t_mark, uint
                 }
             } else {
                 CUDA_TRY(cudaGraphLaunch(c->graph[parity % 2], c->stream));
-                c->launches += chunk;
+                c->launches += c->graph_kernels;
             }
             n = chunk;
         } else {
