@@ -155,6 +155,16 @@ typedef struct swe_run_result {
     int32_t guard_warnings;
 } swe_run_result;
 
+/* StepAccounting (executor.hpp:218-222), per step of this rank:
+ * halo values received from the strip neighbours, and the predictor /
+ * corrector rows the row-chunked march recomputes at work-item boundaries
+ * (in full-row units). */
+typedef struct swe_accounting {
+    int64_t halo_values_exchanged;
+    int32_t redundant_star_rows;
+    int32_t redundant_corrector_rows;
+} swe_accounting;
+
 /* Early-exit accounting since the last load (SWE_EXEC_EARLY_EXIT). */
 typedef struct swe_activity {
     uint64_t cells_per_step;  /* interior cells of this rank */
@@ -235,6 +245,8 @@ int swe_cuda_advance_marked(swe_ctx* ctx, double t_end, double t_mark, uint64_t 
 double swe_cuda_time(const swe_ctx* ctx);
 int32_t swe_cuda_guard_warnings(const swe_ctx* ctx);
 int swe_cuda_timing(const swe_ctx* ctx, swe_timing* out);
+/* Stepper::accounting (executor.hpp:804) */
+int swe_cuda_accounting(const swe_ctx* ctx, swe_accounting* out);
 /* Early-exit counters (all zero skips when SWE_EXEC_EARLY_EXIT is off). */
 int swe_cuda_activity(swe_ctx* ctx, swe_activity* out);
 /* Rows owned by this rank: [*row_begin, *row_end). */

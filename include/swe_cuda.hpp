@@ -149,12 +149,38 @@ struct ExecutorKind {
     }
 };
 
+// StepTimings (executor.hpp:153-172): the six plan kernels run fused in one
+// launch, so their device time is reported as fused_seconds.
+struct StepTimings {
+    double kernel_seconds[6] = {0, 0, 0, 0, 0, 0};
+    double smooth_seconds = 0.0, exchange_seconds = 0.0, fused_seconds = 0.0;
+    unsigned long long steps = 0;
+    double total() const {
+        double s = smooth_seconds + exchange_seconds + fused_seconds;
+        for (double k : kernel_seconds) s += k;
+        return s;
+    }
+};
+struct StepAccounting {  // executor.hpp:218-222
+    long long halo_values_exchanged = 0;
+    int redundant_star_rows = 0;
+    int redundant_corrector_rows = 0;
+};
+// StepPlan (executor.hpp:134-148): K1..K6 (+ smoothing), all in one launch here
+inline std::vector<std::string> step_plan(bool smoothing) {
+    std::vector<std::string> k = {"k1_ghost_committed", "k2_predictor", "k3_ghost_star", "k4_corrector"};
+    if (smoothing) k.push_back("smooth");
+    k.push_back("k5_guard");
+    k.push_back("k6_dt_reduce");
+    return k;
+}
+
 // ---- swe::Stepper ----------------------------------------------------------
 class Stepper {
 public:
     Stepper(const GridSpec& spec, const PhysicsParams& phys, const StabilityPolicy& pol, const BoundarySet& b,
             const ExecutorKind& kind = ExecutorKind::cuda())
-        : spec_(spec) {
+        : spec_(spec), kind_(kind), nu_art_(phys.nu_art) {
         const swe_grid g{spec.nx, spec.ny, spec.dx, spec.dy};
         const swe_physics p{phys.g, phys.manning_n, phys.nu_art};
         const swe_policy po{pol.cfl, pol.dt_max, pol.dt_min, pol.h_min};
@@ -215,6 +241,22 @@ public:
     }
 
     double time() const { return swe_cuda_time(ctx_); }
+    // executor.hpp:801-804
+    const ExecutorKind& kind() const { return kind_; }
+    std::vector<std::string> plan() const { return step_plan(nu_art_ > 0.0); }
+    StepTimings timings() const {
+        swe_timing t{};
+        swe_cuda_timing(ctx_, &t);
+        StepTimings o;
+        o.fused_seconds = t.step_seconds;
+        o.steps = t.steps;
+        return o;
+    }
+    StepAccounting accounting() const {
+        swe_accounting a{};
+        swe_cuda_accounting(ctx_, &a);
+        return {a.halo_values_exchanged, a.redundant_star_rows, a.redundant_corrector_rows};
+    }
     int guard_warnings() const { return swe_cuda_guard_warnings(ctx_); }
 
     // executor.hpp:812-841
@@ -275,6 +317,8 @@ private:
         return o;
     }
     GridSpec spec_;
+    ExecutorKind kind_;
+    double nu_art_ = 0.0;
     swe_ctx* ctx_ = nullptr;
     int32_t row_begin_ = 0, row_end_ = 0;
     std::vector<double> z_;

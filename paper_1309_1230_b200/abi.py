@@ -88,6 +88,11 @@ class swe_activity(C.Structure):
                 ("eligible_items", C.c_uint64), ("skipped_cells", C.c_uint64)]
 
 
+class swe_accounting(C.Structure):
+    _fields_ = [("halo_values_exchanged", C.c_int64), ("redundant_star_rows", C.c_int32),
+                ("redundant_corrector_rows", C.c_int32)]
+
+
 class swe_timing(C.Structure):
     _fields_ = [("steps", C.c_uint64), ("step_seconds", C.c_double)]
 
@@ -115,6 +120,7 @@ SIGNATURES = {
     "swe_cuda_time": (C.c_double, [C.c_void_p]),
     "swe_cuda_guard_warnings": (C.c_int32, [C.c_void_p]),
     "swe_cuda_timing": (C.c_int, [C.c_void_p, C.POINTER(swe_timing)]),
+    "swe_cuda_accounting": (C.c_int, [C.c_void_p, C.POINTER(swe_accounting)]),
     "swe_cuda_activity": (C.c_int, [C.c_void_p, C.POINTER(swe_activity)]),
     "swe_cuda_rows": (None, [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "swe_cuda_halo_rows": (C.c_int32, [C.c_void_p]),

@@ -1101,6 +1101,7 @@ EXPORT int swe_cuda_create(const swe_grid* grid, const swe_physics* phys, const 
 EXPORT void swe_cuda_destroy(swe_ctx* c) {
     if (!c) return;
     if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->stream_edge) cudaStreamSynchronize(c->stream_edge);
     destroy_graphs(c);
     delete c->tr;
     cudaFree(c->d_xr);
@@ -1651,6 +1652,19 @@ EXPORT int swe_cuda_timing(const swe_ctx* c, swe_timing* out) {
     *out = c->timing;
     return SWE_OK;
 }
+EXPORT int swe_cuda_accounting(const swe_ctx* c, swe_accounting* out) {
+    if (!c || !out) return SWE_ERR_CONFIG;
+    std::memset(out, 0, sizeof *out);
+    const int nb = (c->ex.rank > 0 ? 1 : 0) + (c->ex.rank + 1 < c->ex.nranks ? 1 : 0);
+    out->halo_values_exchanged = static_cast<int64_t>(nb) * c->R * 3 * c->g.nx;
+    if (c->loaded) {  // each work item's march starts R rows early and ends R rows late
+        const int items_per_column = c->overlap ? c->prm_int.nchunks + c->prm_edge.nchunks : c->prm.nchunks;
+        out->redundant_star_rows = items_per_column * 2 * c->R;
+        out->redundant_corrector_rows = items_per_column * 2 * (c->R - 1);
+    }
+    return SWE_OK;
+}
+
 EXPORT void swe_cuda_rows(const swe_ctx* c, int32_t* row_begin, int32_t* row_end) {
     if (row_begin) *row_begin = c ? c->j0 : 0;
     if (row_end) *row_end = c ? c->j0 + c->nloc : 0;

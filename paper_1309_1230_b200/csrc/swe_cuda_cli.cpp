@@ -320,6 +320,7 @@ struct Report {
     unsigned long long steps = 0;
     double t_final = 0.0, wall = 0.0, device_step_seconds = 0.0;
     long long halo_values = 0;
+    int redundant_star_rows = 0, redundant_corrector_rows = 0;
     int snapshots = 0, clamp_warnings = 0;
     std::vector<std::string> paths;
     std::string text() const {
@@ -333,8 +334,10 @@ struct Report {
                               "k6_dt_reduce"})
             os << k << "_seconds: 0\n";
         os << "smooth_seconds: 0\nhalo_exchange_seconds: 0\nfused_step_seconds: " << short_double(device_step_seconds)
-           << "\nhalo_values_exchanged_per_step: " << halo_values << "\nredundant_predictor_rows_per_step: 0"
-           << "\nredundant_corrector_rows_per_step: 0\nsnapshots_written: " << snapshots << "\n";
+           << "\nhalo_values_exchanged_per_step: " << halo_values
+           << "\nredundant_predictor_rows_per_step: " << redundant_star_rows
+           << "\nredundant_corrector_rows_per_step: " << redundant_corrector_rows << "\nsnapshots_written: " << snapshots
+           << "\n";
         if (clamp_warnings > 0)
             os << "warning: fixed-elevation boundary clamped ghost depth to h_min (" << clamp_warnings << " fills)\n";
         return os.str();
@@ -438,7 +441,12 @@ Report run_scenario(const Scenario& sc, bool write) {
                 swe_timing tm{};
                 swe_cuda_timing(st.handle(), &tm);
                 rep.device_step_seconds = tm.step_seconds;
-                rep.halo_values = static_cast<long long>(nr - 1) * 2 * swe_cuda_halo_rows(st.handle()) * 3 * sc.nx;
+                rep.redundant_star_rows = st.accounting().redundant_star_rows;
+                rep.redundant_corrector_rows = st.accounting().redundant_corrector_rows;
+            }
+            {  // StepAccounting summed over ranks, like the reference's decomposed bands
+                std::lock_guard<std::mutex> lk(m);
+                rep.halo_values += st.accounting().halo_values_exchanged;
             }
             if (!std::isfinite(dt_raw)) dt_raw = 0.0;
             snap(dt_raw, true);

@@ -373,6 +373,18 @@ class Stepper:
         self._lib.swe_cuda_timing(self._ctx, C.byref(t))
         return t.steps, t.step_seconds
 
+    def accounting(self) -> dict:
+        """StepAccounting (executor.hpp:218-222, 804) of this rank, per step."""
+        a = abi.swe_accounting()
+        self._lib.swe_cuda_accounting(self._ctx, C.byref(a))
+        return {"halo_values_exchanged": a.halo_values_exchanged, "redundant_star_rows": a.redundant_star_rows,
+                "redundant_corrector_rows": a.redundant_corrector_rows}
+
+    def plan(self) -> list:
+        """StepPlan::standard(nu_art > 0) (executor.hpp:134-148); one fused launch runs all of it."""
+        k = ["k1_ghost_committed", "k2_predictor", "k3_ghost_star", "k4_corrector"]
+        return k + (["smooth"] if self.phys.nu_art > 0 else []) + ["k5_guard", "k6_dt_reduce"]
+
     def activity(self) -> dict:
         """Early-exit counters since the last load (swe_cuda_activity)."""
         a = abi.swe_activity()

@@ -51,6 +51,7 @@ def run_strips(sc, nranks, exact, steps, early=False, api="advance"):
     results = [None] * nranks
     states = [None] * nranks
     launches = [0] * nranks
+    acc = [None] * nranks
     errors = []
 
     def worker(r):
@@ -66,6 +67,7 @@ def run_strips(sc, nranks, exact, steps, early=False, api="advance"):
             st.state_rows(h, qx, qy)
             states[r] = (r0, r1, h, qx, qy, st.time())
             launches[r] = st.launch_count()
+            acc[r] = st.accounting()
             st.close()
         except Exception as e:  # surfaced by the caller
             errors.append((r, repr(e)))
@@ -81,6 +83,7 @@ def run_strips(sc, nranks, exact, steps, early=False, api="advance"):
         fs.h[r0:r1], fs.qx[r0:r1], fs.qy[r0:r1], fs.t = h, qx, qy, t
     assert all(x == results[0] for x in results), results  # every rank sees the same outcome
     run_strips.launches = launches
+    run_strips.accounting = acc
     return fs, results[0]
 
 
@@ -114,6 +117,10 @@ def test_strips_bit_identical_exact(name, nranks):
     # group's allreduce kernel
     rows = sc.spec.ny // nranks
     assert all(n == (4 if rows >= 32 else 3) * 60 for n in run_strips.launches), run_strips.launches
+    # StepAccounting: R halo rows of h, qx, qy from each neighbour
+    R = 2 if sc.phys.nu_art > 0 else 1
+    halo = [a["halo_values_exchanged"] for a in run_strips.accounting]
+    assert halo == [(1 if r in (0, nranks - 1) else 2) * R * 3 * sc.spec.nx for r in range(nranks)]
 
 
 @pytest.mark.parametrize("name", sorted(SCEN))
