@@ -28,6 +28,7 @@
 #include <filesystem>
 #include <fstream>
 #include <iostream>
+#include <iterator>
 #include <mutex>
 #include <sstream>
 #include <string>
@@ -304,6 +305,44 @@ void write_snapshot(const FieldSet& fs, const std::string& path, double g, doubl
         throw IoError("cannot write snapshot '" + path + "'");
 }
 
+// read_snapshot (io.hpp:142-241): header, four blocks, trailing resume records
+struct Resume {
+    FieldSet fs;
+    bool has_dt = false, has_idx = false;
+    double dt_next = 0.0;
+    unsigned long long step_index = 0;
+};
+
+Resume read_snapshot(const std::string& path) {
+    std::ifstream f(path, std::ios::binary);
+    if (!f) throw IoError("cannot open snapshot '" + path + "'");
+    const std::string b((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+    if (b.size() < 56) throw IoError("snapshot: truncated header");
+    if (b.compare(0, 4, "SWS1") != 0) throw IoError("snapshot: bad magic");
+    uint32_t hdr[3];
+    double hf[5];
+    std::memcpy(hdr, b.data() + 4, sizeof hdr);
+    std::memcpy(hf, b.data() + 16, sizeof hf);
+    if (hdr[0] != 1u) throw IoError("snapshot: unsupported version");
+    const std::size_t n = static_cast<std::size_t>(hdr[1]) * hdr[2];
+    if (b.size() < 56 + 32 * n) throw IoError("snapshot: truncated payload");
+    Resume r;
+    r.fs = FieldSet(GridSpec(static_cast<int>(hdr[1]), static_cast<int>(hdr[2]), hf[0], hf[1]));
+    r.fs.t = hf[2];
+    std::vector<double>* blocks[4] = {&r.fs.z, &r.fs.h, &r.fs.qx, &r.fs.qy};
+    for (int k = 0; k < 4; ++k) std::memcpy(blocks[k]->data(), b.data() + 56 + 8 * n * k, 8 * n);
+    for (std::size_t off = 56 + 32 * n; off < b.size(); off += 12) {
+        if (b.size() - off < 12) throw IoError("snapshot: truncated trailing record");
+        uint32_t tag;
+        double v;
+        std::memcpy(&tag, b.data() + off, 4);
+        std::memcpy(&v, b.data() + off + 4, 8);
+        if (tag == 1u) r.has_dt = true, r.dt_next = v;
+        if (tag == 2u) r.has_idx = true, r.step_index = static_cast<unsigned long long>(v);
+    }
+    return r;
+}
+
 std::string short_double(double d) {  // shortest round-tripping form (io.hpp fmt_double_short)
     char b[40];
     for (int p = 15; p <= 17; ++p) {
@@ -350,13 +389,17 @@ std::string snapshot_path(const Scenario& sc, int ordinal, bool final) {
     return sc.out_dir + "/" + sc.name + (final ? std::string("_final") : "_" + std::string(b)) + ".sws";
 }
 
-Report run_scenario(const Scenario& sc, bool write) {
+// run / run_from (run.hpp:101-179): from the scenario's initial state, or from
+// a snapshot with its resume records (step parity and raw dt travel with it)
+Report run_scenario(const Scenario& sc, bool write, const Resume* resume = nullptr) {
     const Exec& ex = sc.exec;
     const int nr = ex.ranks;
     const GridSpec spec(sc.nx, sc.ny, sc.dx, sc.dy);
     if (write) std::filesystem::create_directories(sc.out_dir);
-    const bool device_ic = sc.ic.kind == IC_FLAT || sc.ic.kind == IC_CHANNEL || sc.ic.kind == IC_DAM;
-    FieldSet host = device_ic ? FieldSet() : host_initial(sc);
+    if (resume && (resume->fs.spec.nx != sc.nx || resume->fs.spec.ny != sc.ny))
+        throw ConfigError("resume: snapshot grid does not match the config");
+    const bool device_ic = !resume && (sc.ic.kind == IC_FLAT || sc.ic.kind == IC_CHANNEL || sc.ic.kind == IC_DAM);
+    FieldSet host = resume ? resume->fs : device_ic ? FieldSet() : host_initial(sc);
     FieldSet shared(spec);  // gathered committed state for snapshots
     Report rep;
     rep.scenario = sc.name;
@@ -393,15 +436,18 @@ Report run_scenario(const Scenario& sc, bool write) {
                 st.load_initial(ic, 0.0);
             } else {
                 st.load(host);
-                try {  // build_initial_state's own guard (scenarios.hpp:165-169)
-                    st.guard();
-                } catch (const InstabilityError& e) {
-                    throw ConfigError(std::string("initial state fails the stability guard: ") + e.what());
+                if (!resume) {
+                    try {  // build_initial_state's own guard (scenarios.hpp:165-169)
+                        st.guard();
+                    } catch (const InstabilityError& e) {
+                        throw ConfigError(std::string("initial state fails the stability guard: ") + e.what());
+                    }
                 }
             }
             st.guard();  // run_from's precondition (run.hpp:106-109)
-            unsigned long long sidx = 0, steps = 0;
-            double t = 0.0, dt_raw = std::numeric_limits<double>::quiet_NaN();
+            unsigned long long sidx = resume && resume->has_idx ? resume->step_index : 0, steps = 0;
+            double t = resume ? resume->fs.t : 0.0;
+            double dt_raw = resume && resume->has_dt ? resume->dt_next : std::numeric_limits<double>::quiet_NaN();
             const double se = sc.snapshot_every;
             double mark = se > 0.0 ? (std::floor(t / se) + 1.0) * se : std::numeric_limits<double>::infinity();
             int ordinal = 0;
@@ -564,7 +610,7 @@ std::string slurp(const std::string& path) {
 
 void usage() {
     std::cerr << "usage: swe_cuda run --config FILE [--set section.key=value]... [--executor SPEC] [--out DIR]\n"
-                 "                    [--snapshot-every S] [--quiet]\n"
+                 "                    [--snapshot-every S] [--resume SNAPSHOT.sws] [--quiet]\n"
                  "       swe_cuda bench [--sizes 256,512] [--steps 50] [--executors cuda,cuda:fast] [--reps 3]\n"
                  "                      [--csv bench.csv]\n"
                  "SPEC: cuda[:N][:fast|:exact][:early][:local] (naive|tiled|decomposed run as exact cuda)\n";
@@ -585,7 +631,7 @@ int main(int argc, char** argv) {
     };
     try {
         if (cmd == "run") {
-            std::string config, exec, out;
+            std::string config, exec, out, resume_path;
             std::vector<std::string> sets;
             double se = -1.0;
             bool quiet = false;
@@ -596,6 +642,7 @@ int main(int argc, char** argv) {
                 else if (a[k] == "--out") out = opt(k);
                 else if (a[k] == "--snapshot-every") se = std::stod(opt(k));
                 else if (a[k] == "--quiet") quiet = true;
+                else if (a[k] == "--resume") resume_path = opt(k);
                 else throw ConfigError("unknown option '" + a[k] + "'");
             }
             if (config.empty()) throw ConfigError("run: --config is required");
@@ -611,7 +658,9 @@ int main(int argc, char** argv) {
             if (!exec.empty()) sc.exec = parse_exec_spec(exec);
             if (!out.empty()) sc.out_dir = out;
             if (se >= 0.0) sc.snapshot_every = se;
-            const Report r = run_scenario(sc, true);
+            Resume res;
+            if (!resume_path.empty()) res = read_snapshot(resume_path);
+            const Report r = run_scenario(sc, true, resume_path.empty() ? nullptr : &res);
             if (!quiet) std::cout << r.text() << "final_snapshot: " << r.paths.back() << "\n";
             return 0;
         }

@@ -163,3 +163,43 @@ def test_cli_bench_writes_csv(tmp_path):
     assert rows[0] == "size,executor,steps,reps,median_sec_per_step,cells_per_second"
     assert [l.split(",")[:2] for l in rows[1:]] == [["64", "cuda"], ["64", "cuda:fast"], ["96", "cuda"],
                                                     ["96", "cuda:fast"]]
+
+
+DROPS48_CKPT = """
+[grid]
+nx = 48
+ny = 48
+[policy]
+cfl = 0.45
+[initial]
+kind = drops
+depth = 1
+drop = 23.5 23.5 2.4 0.3
+drop = 11.5 11.5 2.4 0.3
+drop = 35.5 11.5 2.4 0.3
+[run]
+name = ckpt
+t_end = 6
+snapshot_every = 2
+"""
+
+
+@pytest.mark.parametrize("text,which", [(DROPS48_CKPT, 0),
+                                        (DAM_CHANNEL.replace("t_end = 15.96", "t_end = 15.96\nsnapshot_every = 3.99"),
+                                         1)])
+def test_cli_checkpoint_resume_is_bit_exact(text, which, tmp_path):
+    """test_io.cpp:268-315: resuming from an intermediate snapshot (its dt_next
+    and step_index records) reproduces the unsplit run's final state bytes."""
+    full, res = tmp_path / "full", tmp_path / "resumed"
+    r = run_cli(text, full, tmp_path)
+    assert r.returncode == 0, r.stderr
+    mids = [f for f in sws_files(full) if not f.endswith("_final.sws")]
+    assert len(mids) > which
+    r = run_cli(text, res, tmp_path, "--resume", str(full / mids[which]))
+    assert r.returncode == 0, r.stderr
+    name = [f for f in sws_files(full) if f.endswith("_final.sws")][0]
+    assert (full / name).read_bytes() == (res / name).read_bytes()
+    steps = lambda d: int(dict(l.split(": ", 1) for l in (d / name.replace("_final.sws", "_report.txt"))
+                               .read_text().splitlines() if ": " in l)["steps"])
+    _, _, ex = sio.parse_snapshot((full / mids[which]).read_bytes())
+    assert steps(full) == ex["step_index"] + steps(res)

@@ -272,3 +272,28 @@ def test_launch_count_is_one_kernel_per_step():
     n0 = g.launch_count()
     g.advance(1e18, 0, math.nan, 128)
     assert g.launch_count() - n0 == 128
+
+
+@pytest.mark.parametrize("edge", ["north", "south", "east", "west"])
+@pytest.mark.parametrize("kind", [EXACT, FAST], ids=["exact", "fast"])
+def test_inflow_admits_the_prescribed_volume_on_every_edge(edge, kind):
+    """test_executor.cpp:192-222: one inflow edge at a time, 60 steps; the added
+    volume equals q_n * edge length * t to 1e-12."""
+    spec = GridSpec(24, 18, 1.0, 1.0)
+    fs = FieldSet(spec)
+    fs.h[:] = 1.0
+    walls = dict(north=BoundaryKind.wall(), south=BoundaryKind.wall(), east=BoundaryKind.wall(),
+                 west=BoundaryKind.wall())
+    walls[edge] = BoundaryKind.inflow(0.05, 1.0)
+    bounds = BoundarySet(**walls)
+    pol = StabilityPolicy(cfl=0.45)
+    st = Stepper(spec, PhysicsParams(), pol, bounds, kind)
+    st.load(fs)
+    dt = st.compute_dt(1e18)
+    t = 0.0
+    for k in range(60):
+        t += dt
+        dt = st.step(dt, k).dt_next
+    added = st.state().h.sum() - fs.h.sum()
+    edge_len = 18.0 if edge in ("east", "west") else 24.0
+    assert abs(added - 0.05 * edge_len * t) <= 1e-12 * (0.05 * edge_len * t)
