@@ -1057,7 +1057,7 @@ EXPORT int swe_cuda_create(const swe_grid* grid, const swe_physics* phys, const 
     {
         std::string err;
         for (int k = 0; k < 2; ++k)
-            if (!encode_rows(&p.tmap_state[k], c->d_buf[k], c->pitch, static_cast<long long>(rows) * 3, 3 * SWE_ROW_GROUP, err))
+            if (!encode_rows(&p.tmap_state[k], c->d_buf[k], c->pitch, static_cast<long long>(rows) * 3, 3 * swe_row_group(c->exact), err))
                 return set_status(st, SWE_ERR_RUNTIME, -1, -1, 0, "%s", err.c_str());
     }
     p.buf[0] = c->d_buf[0];
@@ -1205,7 +1205,7 @@ int finish_load(swe_ctx* c, double t, swe_status* st) {
     c->prm.slope = c->d_slope;
     {
         std::string err;
-        if (!encode_rows(&c->prm.tmap_slope, c->d_slope, P, static_cast<long long>(nloc + 2 * R) * 2, 2 * SWE_ROW_GROUP, err))
+        if (!encode_rows(&c->prm.tmap_slope, c->d_slope, P, static_cast<long long>(nloc + 2 * R) * 2, 2 * swe_row_group(c->exact), err))
             return set_status(st, SWE_ERR_RUNTIME, -1, -1, 0, "%s", err.c_str());
     }
 

@@ -33,7 +33,6 @@
 
 namespace swe_dev {
 
-constexpr int kStages = 4;  // ring depth in row groups (8 rows in flight)
 // Resident CTAs per SM (4 warps each) the register allocation must allow:
 // 4 (16 warps, 128 registers) where the extra warps pay -- exact mode and the
 // flat frictionless step -- and 3 (12 warps, 168 registers) for the fast steps
@@ -46,6 +45,14 @@ constexpr int step_min_blocks() {
 #else
     return (EXACT || (FLAT && !MANNING)) ? 4 : 3;
 #endif
+}
+
+// Ring depth in row groups per warp: 8 rows in flight with groups of 2; with
+// groups of 4, as many as fit 227 KB of shared memory at the variant's
+// occupancy (3 stages, 2 for 16 warps on a sloped bed).
+template <bool EXACT, bool FLAT, bool MANNING>
+constexpr int step_stages() {
+    return swe_row_group(EXACT) == 2 ? 4 : (FLAT || step_min_blocks<EXACT, FLAT, MANNING>() == 3) ? 3 : 2;
 }
 
 // ---------------------------------------------------------------- PTX helpers
@@ -93,10 +100,10 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
-// Rows per TMA request: one 2D box carries G consecutive rows (state box
-// 32 x 3G, slope box 32 x 2G), so the per-request issue cost (uniform-register
-// setup, mbarrier arm/wait, ring bookkeeping) is paid once per G rows.
-constexpr int kGroup = SWE_ROW_GROUP;
+// Rows per TMA request (swe_row_group): one 2D box carries G consecutive rows
+// (state box 32 x 3G, slope box 32 x 2G), so the per-request issue cost
+// (uniform-register setup, mbarrier arm/wait, ring bookkeeping) is paid once
+// per G rows.
 
 // ------------------------------------------------------------ work partition
 // Worker w (one warp) owns units [w*U/G, (w+1)*U/G) of the unit space
@@ -230,8 +237,8 @@ struct Marcher {
     static constexpr int R = SMOOTH ? 2 : 1;
     static constexpr int S = FWD ? 1 : -1;
     static constexpr int NF = FLAT ? 3 : 5;
-    static constexpr int D = kStages;
-    static constexpr int G = kGroup;
+    static constexpr int D = step_stages<EXACT, FLAT, MANNING>();
+    static constexpr int G = swe_row_group(EXACT);
     static constexpr int SLOT = NF * G * 32;  // doubles per ring slot: [G][3][32] state, [G][2][32] slopes
     static constexpr int TW = 32 - 2 * R;
     static constexpr unsigned FULL = 0xffffffffu;
@@ -338,7 +345,7 @@ struct Marcher {
         }
     }
     // Row GI (in march order) of the current group.  Groups never span two
-    // segments; the march's row count is static modulo G = 2 (see segment()).
+    // segments; the group row of each march iteration is static (see march()).
     template <int GI>
     __device__ __forceinline__ void consume(CellVec& u, double& zx, double& zy) {
         if constexpr (GI == 0) mbar_wait(&bars[ring.d], ring.ph);
@@ -722,34 +729,49 @@ struct Marcher {
         A.Hyp = {0.0, 0.0, 0.0};
         A.Cp = {0.0, 0.0, 0.0};
         A.Cpp = {0.0, 0.0, 0.0};
-        // corrector of row b in the same iteration as its predictor
+        // corrector of row b in the same iteration as its predictor.  Row GI of
+        // a group is static: the prologue consumes 2 (R = 1) or 4 (R = 2) rows.
+        constexpr int GI0 = (SMOOTH ? 4 : 2) % G;  // group row of the first steady iteration
         int k;
         if constexpr (!SMOOTH) {
             iter<EDGE, true, false, false, 1>(-1, A, B);  // U* of the halo row
             k = 0;                                         // 0..L-1: full iterations
         } else {
-            iter<EDGE, true, false, false, 1>(-2, A, B);  // U* of the outer halo row
-            iter<EDGE, true, true, false, 0>(-1, B, A);   // corrector of the halo row
-            iter<EDGE, true, true, false, 1>(0, A, B);    // first own row: its smoothing waits a row
-            k = 1;                                         // 1..L: smooth + emit row b - S
+            iter<EDGE, true, false, false, 1>(-2, A, B);      // U* of the outer halo row
+            iter<EDGE, true, true, false, 2 % G>(-1, B, A);   // corrector of the halo row
+            iter<EDGE, true, true, false, 3 % G>(0, A, B);    // first own row: its smoothing waits a row
+            k = 1;                                             // 1..L: smooth + emit row b - S
         }
         const int k_last = SMOOTH ? L : L - 1;
-        // carries enter the steady state in B; iterations pair as (B->A GI 0, A->B GI 1)
-        for (; k + 1 <= k_last; k += 2) {
-            iter<EDGE, true, true, true, 0>(k, B, A);
-            iter<EDGE, true, true, true, 1>(k + 1, A, B);
+        const int k_first = k;
+        // carries enter the steady state in B and alternate (B->A, A->B, ...)
+        for (; k + G - 1 <= k_last; k += G) {
+            iter<EDGE, true, true, true, (GI0 + 0) % G>(k, B, A);
+            iter<EDGE, true, true, true, (GI0 + 1) % G>(k + 1, A, B);
+            if constexpr (G == 4) {
+                iter<EDGE, true, true, true, (GI0 + 2) % G>(k + 2, B, A);
+                iter<EDGE, true, true, true, (GI0 + 3) % G>(k + 3, A, B);
+            }
         }
-        if (k <= k_last) {  // odd steady count: release the half-consumed last group
-            iter<EDGE, true, true, true, 0>(k, B, A);
-            next_group();
+        const int rem = k_last - k + 1;  // 0 .. G-1 tail iterations
+        if (rem > 0) {
+            iter<EDGE, true, true, true, (GI0 + 0) % G>(k, B, A);
+            if constexpr (G == 4) {
+                if (rem > 1) {
+                    iter<EDGE, true, true, true, (GI0 + 1) % G>(k + 1, A, B);
+                    if (rem > 2) iter<EDGE, true, true, true, (GI0 + 2) % G>(k + 2, B, A);
+                }
+            }
         }
+        // release a half-consumed last group
+        if ((GI0 + (k_last - k_first + 1) - 1) % G != G - 1) next_group();
     }
 };
 
 template <int WPB, bool FWD, bool SMOOTH, bool FLAT, bool MANNING, bool EXACT, bool EARLY>
 __global__ void __launch_bounds__(WPB * 32, (step_min_blocks<EXACT, FLAT, MANNING>())) swe_step_kernel(const __grid_constant__ StepParams p) {
     using M = Marcher<WPB, FWD, SMOOTH, FLAT, MANNING, EXACT, EARLY>;
-    constexpr int D = kStages;
+    constexpr int D = M::D;
     constexpr int NF = M::NF;
     constexpr unsigned FULL = 0xffffffffu;
 
@@ -957,9 +979,10 @@ __global__ void __launch_bounds__(256) swe_schedule_kernel(const __grid_constant
     }
 }
 
-template <int WPB, bool SMOOTH, bool FLAT>
+template <int WPB, bool SMOOTH, bool FLAT, bool EXACT, bool MANNING>
 constexpr size_t step_smem_bytes() {
-    return static_cast<size_t>(WPB) * kStages * (FLAT ? 3 : 5) * kGroup * 32 * 8 + WPB * kStages * 8;
+    constexpr int D = step_stages<EXACT, FLAT, MANNING>();
+    return static_cast<size_t>(WPB) * D * (FLAT ? 3 : 5) * swe_row_group(EXACT) * 32 * 8 + WPB * D * 8;
 }
 
 }  // namespace swe_dev
