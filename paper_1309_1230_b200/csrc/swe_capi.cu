@@ -1205,7 +1205,13 @@ int finish_load(swe_ctx* c, double t, swe_status* st) {
     c->prm.slope = c->d_slope;
     {
         std::string err;
-        if (!encode_rows(&c->prm.tmap_slope, c->d_slope, P, static_cast<long long>(nloc + 2 * R) * 2, 2 * swe_row_group(c->exact), err))
+        // row-group boxes of the kernels this load selects (early exit needs a flat bed)
+        const int G = swe_row_group(c->exact, c->early && c->flat);
+        for (int k = 0; k < 2; ++k)
+            if (!encode_rows(&c->prm.tmap_state[k], c->d_buf[k], P, static_cast<long long>(nloc + 2 * R) * 3, 3 * G,
+                             err))
+                return set_status(st, SWE_ERR_RUNTIME, -1, -1, 0, "%s", err.c_str());
+        if (!encode_rows(&c->prm.tmap_slope, c->d_slope, P, static_cast<long long>(nloc + 2 * R) * 2, 2 * G, err))
             return set_status(st, SWE_ERR_RUNTIME, -1, -1, 0, "%s", err.c_str());
     }
 

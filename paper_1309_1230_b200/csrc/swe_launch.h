@@ -12,8 +12,9 @@
 #define SWE_TILE_W(R) (32 - 2 * (R))  // output columns per warp window
 // Rows per TMA request (state box 32 x 3G, slope box 32 x 2G): 4 in fast mode
 // (fewer request and ring-bookkeeping instructions per cell: 3-5 % faster),
-// 2 in exact mode (its larger kernels spill with the deeper ring).
-constexpr int swe_row_group(bool exact) { return exact ? 2 : 4; }
+// 2 in exact mode (its larger kernels spill with the deeper ring) and for the
+// early-exit kernels (short 32-row items).
+constexpr int swe_row_group(bool exact, bool early = false) { return (exact || early) ? 2 : 4; }
 
 // bit 16: early-exit instantiation (flat bed only)
 inline int swe_step_variant(bool fwd, bool smooth, bool flat, bool manning, bool early = false) {

@@ -50,9 +50,9 @@ constexpr int step_min_blocks() {
 // Ring depth in row groups per warp: 8 rows in flight with groups of 2; with
 // groups of 4, as many as fit 227 KB of shared memory at the variant's
 // occupancy (3 stages, 2 for 16 warps on a sloped bed).
-template <bool EXACT, bool FLAT, bool MANNING>
+template <bool EXACT, bool FLAT, bool MANNING, bool EARLY>
 constexpr int step_stages() {
-    return swe_row_group(EXACT) == 2 ? 4 : (FLAT || step_min_blocks<EXACT, FLAT, MANNING>() == 3) ? 3 : 2;
+    return swe_row_group(EXACT, EARLY) == 2 ? 4 : (FLAT || step_min_blocks<EXACT, FLAT, MANNING>() == 3) ? 3 : 2;
 }
 
 // ---------------------------------------------------------------- PTX helpers
@@ -237,8 +237,8 @@ struct Marcher {
     static constexpr int R = SMOOTH ? 2 : 1;
     static constexpr int S = FWD ? 1 : -1;
     static constexpr int NF = FLAT ? 3 : 5;
-    static constexpr int D = step_stages<EXACT, FLAT, MANNING>();
-    static constexpr int G = swe_row_group(EXACT);
+    static constexpr int D = step_stages<EXACT, FLAT, MANNING, EARLY>();
+    static constexpr int G = swe_row_group(EXACT, EARLY);
     static constexpr int SLOT = NF * G * 32;  // doubles per ring slot: [G][3][32] state, [G][2][32] slopes
     static constexpr int TW = 32 - 2 * R;
     static constexpr unsigned FULL = 0xffffffffu;
@@ -979,10 +979,10 @@ __global__ void __launch_bounds__(256) swe_schedule_kernel(const __grid_constant
     }
 }
 
-template <int WPB, bool SMOOTH, bool FLAT, bool EXACT, bool MANNING>
+template <int WPB, bool SMOOTH, bool FLAT, bool EXACT, bool MANNING, bool EARLY>
 constexpr size_t step_smem_bytes() {
-    constexpr int D = step_stages<EXACT, FLAT, MANNING>();
-    return static_cast<size_t>(WPB) * D * (FLAT ? 3 : 5) * swe_row_group(EXACT) * 32 * 8 + WPB * D * 8;
+    constexpr int D = step_stages<EXACT, FLAT, MANNING, EARLY>();
+    return static_cast<size_t>(WPB) * D * (FLAT ? 3 : 5) * swe_row_group(EXACT, EARLY) * 32 * 8 + WPB * D * 8;
 }
 
 }  // namespace swe_dev

@@ -40,7 +40,7 @@ constexpr bool kSmooth = (SWE_PART & 1) != 0;
 
 template <bool FLAT, bool MANNING, bool EARLY>
 cudaError_t launch_one(int grid, cudaStream_t s, const StepParams& p) {
-    constexpr size_t smem = swe_dev::step_smem_bytes<kWPB, kSmooth, FLAT, kExact, MANNING>();
+    constexpr size_t smem = swe_dev::step_smem_bytes<kWPB, kSmooth, FLAT, kExact, MANNING, EARLY>();
     auto k = swe_dev::swe_step_kernel<kWPB, kFwd, kSmooth, FLAT, MANNING, kExact, EARLY>;
     static bool configured = false;
     if (!configured) {
@@ -55,7 +55,7 @@ cudaError_t launch_one(int grid, cudaStream_t s, const StepParams& p) {
 
 template <bool FLAT, bool MANNING, bool EARLY>
 int occupancy_one() {
-    constexpr size_t smem = swe_dev::step_smem_bytes<kWPB, kSmooth, FLAT, kExact, MANNING>();
+    constexpr size_t smem = swe_dev::step_smem_bytes<kWPB, kSmooth, FLAT, kExact, MANNING, EARLY>();
     auto k = swe_dev::swe_step_kernel<kWPB, kFwd, kSmooth, FLAT, MANNING, kExact, EARLY>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     int n = 0;
