@@ -156,6 +156,7 @@ __global__ void slopes_kernel(const double* zp, double* slope, int P, int R, int
             sx = (zat(ie, j) - zat(iw, j)) / two_dx;
             sy = (zat(i, jn) - zat(i, js)) / two_dy;
             if (swe_dev::dbits(sx) != 0ull || swe_dev::dbits(sy) != 0ull) atomicOr(flags, 1u);
+            if (swe_dev::dbits(sy) != 0ull) atomicOr(flags + 2, 1u);
         }
         slope[(static_cast<size_t>(lr + R) * 2 + 0) * P + (i + R)] = sx;
         slope[(static_cast<size_t>(lr + R) * 2 + 1) * P + (i + R)] = sy;
@@ -303,7 +304,10 @@ __global__ void scan_kernel(const double* b, int P, int R, int nx, int nloc, int
 // ---------------------------------------------------------------- TMA descriptors
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
-bool encode_rows(CUtensorMap* map, double* base, int P, long long field_rows, int box_rows, std::string& err) {
+// 2D map over field_rows rows of P doubles at row_stride doubles (P if 0); box
+// box_cols x box_rows
+bool encode_rows(CUtensorMap* map, double* base, int P, long long field_rows, int box_rows, std::string& err,
+                 int box_cols = 32, int row_stride = 0) {
     if (!g_encode) {
         cudaDriverEntryPointQueryResult q;
         void* fn = nullptr;
@@ -315,8 +319,8 @@ bool encode_rows(CUtensorMap* map, double* base, int P, long long field_rows, in
         g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     }
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(P), static_cast<cuuint64_t>(field_rows)};
-    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(P) * sizeof(double)};
-    const cuuint32_t box[2] = {32u, static_cast<cuuint32_t>(box_rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(row_stride > 0 ? row_stride : P) * sizeof(double)};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
     const cuuint32_t estr[2] = {1u, 1u};
     const CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, base, dims, strides, box, estr,
                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -410,7 +414,7 @@ struct swe_ctx {
     swe_boundary_set bnd{};
     swe_exec ex{};
     int R = 1, nloc = 0, j0 = 0, pitch = 0, ntiles = 0;
-    bool smooth = false, manning = false, flat = true, loaded = false, exact = true;
+    bool smooth = false, manning = false, flat = true, xonly = false, loaded = false, exact = true;
     int clamp_any = 0;
     int warnings_total = 0;
     double t = 0.0;
@@ -726,7 +730,7 @@ int halo_exchange(swe_ctx* c, int which, cudaStream_t s, swe_status* st) {
 // `cand` = candidate buffer as assumed by the host (used for the strip halo
 // exchange only).
 int enqueue_step(swe_ctx* c, bool fwd, int cand, swe_status* st) {
-    const int v = swe_step_variant(fwd, c->smooth, c->flat, c->manning, c->early);
+    const int v = swe_step_variant(fwd, c->smooth, c->flat, c->manning, c->early, c->xonly);
     if (c->overlap) {
         // Strips, overlapped: the edge launch (the bands whose rows the
         // neighbours need) runs on a high-priority stream and its halo
@@ -1197,10 +1201,11 @@ int finish_load(swe_ctx* c, double t, swe_status* st) {
                                                             b, c->pol.h_min, c->d_flags + 1);
         CUDA_TRY(cudaGetLastError());
     }
-    unsigned flags[2] = {0u, 0u};
+    unsigned flags[3] = {0u, 0u, 0u};
     CUDA_TRY(cudaMemcpyAsync(flags, c->d_flags, sizeof flags, cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     c->flat = (flags[0] == 0);
+    c->xonly = !c->flat && flags[2] == 0;  // every dz/dy is +0.0: skip those rows
     int clamp = flags[1] ? 1 : 0;
     c->prm.slope = c->d_slope;
     {
@@ -1212,6 +1217,8 @@ int finish_load(swe_ctx* c, double t, swe_status* st) {
                              err))
                 return set_status(st, SWE_ERR_RUNTIME, -1, -1, 0, "%s", err.c_str());
         if (!encode_rows(&c->prm.tmap_slope, c->d_slope, P, static_cast<long long>(nloc + 2 * R) * 2, 2 * G, err))
+            return set_status(st, SWE_ERR_RUNTIME, -1, -1, 0, "%s", err.c_str());
+        if (!encode_rows(&c->prm.tmap_slopex, c->d_slope, P, static_cast<long long>(nloc + 2 * R), G, err, 32, 2 * P))
             return set_status(st, SWE_ERR_RUNTIME, -1, -1, 0, "%s", err.c_str());
     }
 
@@ -1236,7 +1243,7 @@ int finish_load(swe_ctx* c, double t, swe_status* st) {
     c->clamp_any = clamp;
 
     // occupancy-sized persistent grid
-    const int v = swe_step_variant(true, c->smooth, c->flat, c->manning, c->early);
+    const int v = swe_step_variant(true, c->smooth, c->flat, c->manning, c->early, c->xonly);
     c->occ = swe_step_occupancy(c->exact, v);
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->ex.device);

@@ -16,9 +16,11 @@
 // early-exit kernels (short 32-row items).
 constexpr int swe_row_group(bool exact, bool early = false) { return (exact || early) ? 2 : 4; }
 
-// bit 16: early-exit instantiation (flat bed only)
-inline int swe_step_variant(bool fwd, bool smooth, bool flat, bool manning, bool early = false) {
-    return (fwd ? 8 : 0) | (smooth ? 4 : 0) | (flat ? 2 : 0) | (manning ? 1 : 0) | ((early && flat) ? 16 : 0);
+// bit 16: early-exit instantiation (flat bed only); bit 32: sloped bed whose
+// dz/dy is +0.0 everywhere (only the dz/dx rows are read)
+inline int swe_step_variant(bool fwd, bool smooth, bool flat, bool manning, bool early = false, bool xonly = false) {
+    return (fwd ? 8 : 0) | (smooth ? 4 : 0) | (flat ? 2 : 0) | (manning ? 1 : 0) | ((early && flat) ? 16 : 0) |
+           ((xonly && !flat) ? 32 : 0);
 }
 cudaError_t swe_launch_step_exact(int variant, int grid, cudaStream_t stream, const StepParams& p);
 cudaError_t swe_launch_step_fast(int variant, int grid, cudaStream_t stream, const StepParams& p);

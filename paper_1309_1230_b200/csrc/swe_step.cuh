@@ -230,13 +230,17 @@ struct WarpRing {  // per-warp TMA ring state (warp-uniform)
     unsigned ph;   // its mbarrier phase parity
 };
 
-template <int WPB, bool FWD, bool SMOOTH, bool FLAT, bool MANNING, bool EXACT, bool EARLY>
+// BED: 0 flat (no bed reads), 1 both slopes, 2 dz/dx only (dz/dy is +0.0
+// everywhere, e.g. a channel sloping along x: the dz/dy rows are not read)
+template <int WPB, bool FWD, bool SMOOTH, int BED, bool MANNING, bool EXACT, bool EARLY>
 struct Marcher {
+    static constexpr bool FLAT = BED == 0;
+    static constexpr bool XONLY = BED == 2;
     using A = Arith<EXACT>;
     using Rc = typename A::Rc;
     static constexpr int R = SMOOTH ? 2 : 1;
     static constexpr int S = FWD ? 1 : -1;
-    static constexpr int NF = FLAT ? 3 : 5;
+    static constexpr int NF = FLAT ? 3 : XONLY ? 4 : 5;  // doubles per cell in the ring
     static constexpr int D = step_stages<EXACT, FLAT, MANNING, EARLY>();
     static constexpr int G = swe_row_group(EXACT, EARLY);
     static constexpr int SLOT = NF * G * 32;  // doubles per ring slot: [G][3][32] state, [G][2][32] slopes
@@ -337,7 +341,8 @@ struct Marcher {
             if (lane == 0) {
                 mbar_expect_tx(&bars[d], SLOT * 8);
                 tma_load_2d(stage + d * SLOT, &p.tmap_state[sel], px, py * 3, &bars[d]);
-                if constexpr (!FLAT) tma_load_2d(stage + d * SLOT + 3 * G * 32, &p.tmap_slope, px, py * 2, &bars[d]);
+                if constexpr (XONLY) tma_load_2d(stage + d * SLOT + 3 * G * 32, &p.tmap_slopex, px, py, &bars[d]);
+                else if constexpr (!FLAT) tma_load_2d(stage + d * SLOT + 3 * G * 32, &p.tmap_slope, px, py * 2, &bars[d]);
             }
             py += S * G;
             --pleft;
@@ -354,7 +359,10 @@ struct Marcher {
         u.h = st[g * 96 + lane];
         u.qx = st[g * 96 + 32 + lane];
         u.qy = st[g * 96 + 64 + lane];
-        if constexpr (!FLAT) {
+        if constexpr (XONLY) {
+            zx = st[G * 96 + g * 32 + lane];
+            zy = 0.0;  // the bed's dz/dy bit patterns are all +0.0
+        } else if constexpr (!FLAT) {
             zx = st[G * 96 + g * 64 + lane];
             zy = st[G * 96 + g * 64 + 32 + lane];
         } else {
@@ -768,9 +776,9 @@ struct Marcher {
     }
 };
 
-template <int WPB, bool FWD, bool SMOOTH, bool FLAT, bool MANNING, bool EXACT, bool EARLY>
-__global__ void __launch_bounds__(WPB * 32, (step_min_blocks<EXACT, FLAT, MANNING>())) swe_step_kernel(const __grid_constant__ StepParams p) {
-    using M = Marcher<WPB, FWD, SMOOTH, FLAT, MANNING, EXACT, EARLY>;
+template <int WPB, bool FWD, bool SMOOTH, int BED, bool MANNING, bool EXACT, bool EARLY>
+__global__ void __launch_bounds__(WPB * 32, (step_min_blocks<EXACT, BED == 0, MANNING>())) swe_step_kernel(const __grid_constant__ StepParams p) {
+    using M = Marcher<WPB, FWD, SMOOTH, BED, MANNING, EXACT, EARLY>;
     constexpr int D = M::D;
     constexpr int NF = M::NF;
     constexpr unsigned FULL = 0xffffffffu;
@@ -979,10 +987,11 @@ __global__ void __launch_bounds__(256) swe_schedule_kernel(const __grid_constant
     }
 }
 
-template <int WPB, bool SMOOTH, bool FLAT, bool EXACT, bool MANNING, bool EARLY>
+template <int WPB, bool SMOOTH, int BED, bool EXACT, bool MANNING, bool EARLY>
 constexpr size_t step_smem_bytes() {
-    constexpr int D = step_stages<EXACT, FLAT, MANNING, EARLY>();
-    return static_cast<size_t>(WPB) * D * (FLAT ? 3 : 5) * swe_row_group(EXACT, EARLY) * 32 * 8 + WPB * D * 8;
+    constexpr int D = step_stages<EXACT, BED == 0, MANNING, EARLY>();
+    constexpr int NF = BED == 0 ? 3 : BED == 2 ? 4 : 5;
+    return static_cast<size_t>(WPB) * D * NF * swe_row_group(EXACT, EARLY) * 32 * 8 + WPB * D * 8;
 }
 
 }  // namespace swe_dev

@@ -38,10 +38,10 @@ constexpr bool kExact = SWE_EXACT_TU != 0;
 constexpr bool kFwd = (SWE_PART & 2) != 0;
 constexpr bool kSmooth = (SWE_PART & 1) != 0;
 
-template <bool FLAT, bool MANNING, bool EARLY>
+template <int BED, bool MANNING, bool EARLY>
 cudaError_t launch_one(int grid, cudaStream_t s, const StepParams& p) {
-    constexpr size_t smem = swe_dev::step_smem_bytes<kWPB, kSmooth, FLAT, kExact, MANNING, EARLY>();
-    auto k = swe_dev::swe_step_kernel<kWPB, kFwd, kSmooth, FLAT, MANNING, kExact, EARLY>;
+    constexpr size_t smem = swe_dev::step_smem_bytes<kWPB, kSmooth, BED, kExact, MANNING, EARLY>();
+    auto k = swe_dev::swe_step_kernel<kWPB, kFwd, kSmooth, BED, MANNING, kExact, EARLY>;
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -53,10 +53,10 @@ cudaError_t launch_one(int grid, cudaStream_t s, const StepParams& p) {
     return cudaGetLastError();
 }
 
-template <bool FLAT, bool MANNING, bool EARLY>
+template <int BED, bool MANNING, bool EARLY>
 int occupancy_one() {
-    constexpr size_t smem = swe_dev::step_smem_bytes<kWPB, kSmooth, FLAT, kExact, MANNING, EARLY>();
-    auto k = swe_dev::swe_step_kernel<kWPB, kFwd, kSmooth, FLAT, MANNING, kExact, EARLY>;
+    constexpr size_t smem = swe_dev::step_smem_bytes<kWPB, kSmooth, BED, kExact, MANNING, EARLY>();
+    auto k = swe_dev::swe_step_kernel<kWPB, kFwd, kSmooth, BED, MANNING, kExact, EARLY>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     int n = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kWPB * 32, smem) != cudaSuccess) return 1;
@@ -69,14 +69,19 @@ struct Entry {
     LaunchFn launch;
     OccFn occ;
 };
-#define SWE_V(Z, M, E) {launch_one<Z, M, E>, occupancy_one<Z, M, E>}
-// index: flat (bit 1) | manning (bit 0); early-exit kernels exist for a flat bed only
-const Entry kTable[4] = {SWE_V(false, false, false), SWE_V(false, true, false), SWE_V(true, false, false),
-                         SWE_V(true, true, false)};
-const Entry kEarly[2] = {SWE_V(true, false, true), SWE_V(true, true, true)};
+#define SWE_V(B, M, E) {launch_one<B, M, E>, occupancy_one<B, M, E>}
+// index: flat (bit 1) | manning (bit 0); bed 0 flat, 1 both slopes, 2 dz/dx only;
+// early-exit kernels exist for a flat bed only
+const Entry kTable[4] = {SWE_V(1, false, false), SWE_V(1, true, false), SWE_V(0, false, false), SWE_V(0, true, false)};
+const Entry kXonly[2] = {SWE_V(2, false, false), SWE_V(2, true, false)};
+const Entry kEarly[2] = {SWE_V(0, false, true), SWE_V(0, true, true)};
 #undef SWE_V
 
-const Entry& entry(int variant) { return (variant & 16) ? kEarly[variant & 1] : kTable[variant & 3]; }
+const Entry& entry(int variant) {
+    if (variant & 16) return kEarly[variant & 1];
+    if ((variant & 32) && !(variant & 2)) return kXonly[variant & 1];
+    return kTable[variant & 3];
+}
 
 }  // namespace swe_inst<part>_<mode>
 using namespace SWE_MODE_NAME(swe_inst);

@@ -65,6 +65,7 @@ struct StepParams {
     // (box 32 x 3 = h, qx, qy of one row); slopes as [2*(nloc+2R)][P] (box 32 x 2)
     CUtensorMap tmap_state[2];
     CUtensorMap tmap_slope;
+    CUtensorMap tmap_slopex;  // the dz/dx rows only (row stride 2P; box 32 x G)
     double* buf[2];        // committed/candidate state, row-interleaved SoA
     const double* slope;   // dzdx/dzdy rows, same layout; nullptr for a flat bed
     const double* z_w;     // bed z at i=0 per local row

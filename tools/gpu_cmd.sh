@@ -1,3 +1,3 @@
-mkdir -p gpurun_out
-bash tools/full_bench.sh
-bash tools/ncu_full.sh c3 fast c3_fast
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_last.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_last.log
+tail -n 4 gpurun_out/pytest_last.log
+bash tools/ab.sh c3 c3f -- head xs 2>&1
