@@ -757,9 +757,13 @@ int enqueue_step(swe_ctx* c, bool fwd, int cand, swe_status* st) {
     CUDA_TRY(swe_launch_step(c->exact, v, c->ncta, c->stream, c->prm));
     ++c->launches;
     if (c->ex.nranks > 1) {
-        int rc = c->tr->allreduce_max(c, c->stream, c->d_ctl->red, RED_N, st);
+        // same collective order as the overlapped path (send/recv, then the
+        // allreduce): ranks may take different paths (strip heights differ
+        // by one row, early exit depends on the local bed) and NCCL requires
+        // every rank to issue a communicator's operations in the same order
+        int rc = halo_exchange(c, cand, c->stream, st);
         if (rc) return rc;
-        rc = halo_exchange(c, cand, c->stream, st);
+        rc = c->tr->allreduce_max(c, c->stream, c->d_ctl->red, RED_N, st);
         if (rc) return rc;
         CUDA_TRY(swe_launch_finalize(c->stream, c->prm));
         c->launches += 1 + (c->tr->capturable() ? 0 : 1);  // finalize (+ local max kernel)

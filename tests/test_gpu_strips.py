@@ -213,3 +213,15 @@ def test_load_initial_on_strips():
         assert res == rr
         assert bits_equal(fs.h[r0:r1], ref.h[r0:r1]) and bits_equal(fs.qx[r0:r1], ref.qx[r0:r1])
         assert bits_equal(fs.qy[r0:r1], ref.qy[r0:r1]) and bits_equal(fs.z[r0:r1], ref.z[r0:r1])
+
+
+def test_strips_mixing_overlapped_and_plain_steps():
+    """ny = 127 on 4 strips gives bands of 32, 32, 32 and 31 rows: the first
+    three overlap their halo exchange, the last does not -- the collectives
+    must still pair up (same order on every rank) and the result must equal
+    the single domain."""
+    sc = S.gen_square_dam(127, 1.0, 0.5)
+    ref, rr = run_single(sc, True, 40)
+    got, rg = run_strips(sc, 4, True, 40)
+    assert rr == rg and same(ref, got)
+    assert run_strips.launches == [4 * 40, 4 * 40, 4 * 40, 3 * 40]
