@@ -14,7 +14,12 @@
 // (fewer request and ring-bookkeeping instructions per cell: 3-5 % faster),
 // 2 in exact mode (its larger kernels spill with the deeper ring) and for the
 // early-exit kernels (short 32-row items).
-constexpr int swe_row_group(bool exact, bool early = false) { return (exact || early) ? 2 : 4; }
+#ifndef SWE_EXACT_ROW_GROUP
+#define SWE_EXACT_ROW_GROUP 2
+#endif
+constexpr int swe_row_group(bool exact, bool early = false) {
+    return early ? 2 : exact ? SWE_EXACT_ROW_GROUP : 4;
+}
 
 // bit 16: early-exit instantiation (flat bed only); bit 32: sloped bed whose
 // dz/dy is +0.0 everywhere (only the dz/dx rows are read)
