@@ -2,16 +2,11 @@
 //
 // Owns the device state of one swe::Stepper replacement (executor.hpp:726-1116):
 // ping-pong padded buffers, bed slopes, the device control block, CUDA graphs
-// for the device-resident run loop, and (for row strips) the NCCL
-// communicator.  Compiled with -fmad=false like the kernels.
-#include <dlfcn.h>
-
+// for the device-resident run loop, and (for row strips) its transport
+// (swe_transport.cu).  The auxiliary kernels live in swe_aux.cu.  Compiled
+// with -fmad=false like the kernels.
 #include <algorithm>
-#include <chrono>
 #include <cmath>
-#include <condition_variable>
-#include <map>
-#include <mutex>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -20,294 +15,44 @@
 #include <vector>
 
 #include <cudaTypedefs.h>
-#include <nccl.h>
 
-#include "swe_device.cuh"
-#include "swe_launch.h"
+#include "swe_runtime.h"
 
 #define EXPORT extern "C" __attribute__((visibility("default")))
 
-namespace {
+using namespace swe_rt;
 
-// ---------------------------------------------------------------- NCCL (dlopen)
-struct NcclApi {
-    void* h = nullptr;
-    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
-    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
-    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
-    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
-                              cudaStream_t) = nullptr;
-    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
-    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
-    ncclResult_t (*GroupStart)() = nullptr;
-    ncclResult_t (*GroupEnd)() = nullptr;
-    const char* (*GetErrorString)(ncclResult_t) = nullptr;
-    bool load(std::string& err) {
-        if (h) return true;
-        const char* names[] = {"libnccl.so.2", "libnccl.so"};
-        for (const char* n : names) {
-            h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
-            if (h) break;
-        }
-        if (!h) {
-            err = "cannot dlopen libnccl.so.2";
-            return false;
-        }
-#define SWE_SYM(f) f = reinterpret_cast<decltype(f)>(dlsym(h, "nccl" #f))
-        SWE_SYM(GetUniqueId);
-        SWE_SYM(CommInitRank);
-        SWE_SYM(CommDestroy);
-        SWE_SYM(AllReduce);
-        SWE_SYM(Send);
-        SWE_SYM(Recv);
-        SWE_SYM(GroupStart);
-        SWE_SYM(GroupEnd);
-        SWE_SYM(GetErrorString);
-#undef SWE_SYM
-        if (!GetUniqueId || !CommInitRank || !AllReduce || !Send || !Recv || !GroupStart ||
-            !GroupEnd) {
-            err = "libnccl.so.2 lacks required symbols";
-            return false;
-        }
-        return true;
+namespace swe_rt {
+
+int set_status(swe_status* st, int code, int i, int j, double t, const char* fmt, ...) {
+    if (st) {
+        std::memset(st, 0, sizeof *st);
+        st->code = code;
+        st->i = i;
+        st->j = j;
+        st->t = t;
+        va_list ap;
+        va_start(ap, fmt);
+        std::vsnprintf(st->msg, sizeof st->msg, fmt, ap);
+        va_end(ap);
     }
-};
-NcclApi g_nccl;
-
-// ---------------------------------------------------------------- aux kernels
-using swe_dev::CellVec;
-
-__device__ __forceinline__ size_t pidx(int P, int R, int lr, int f, int i) {
-    return (static_cast<size_t>(lr + R) * 3 + f) * P + static_cast<size_t>(i + R);
+    return code;
 }
 
-// Fill the whole padded buffer (every field row, all columns) with a benign
-// wet state so never-consumed padding cells stay finite.
-__global__ void fill_benign_kernel(double* buf, size_t rows3, int P) {
-    const size_t n = rows3 * static_cast<size_t>(P);
-    for (size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; k < n;
-         k += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const size_t row = k / P;
-        buf[k] = (row % 3 == 0) ? 1.0 : 0.0;
-    }
+int ok_status(swe_status* st) {
+    if (st) std::memset(st, 0, sizeof *st);
+    return SWE_OK;
 }
 
-// K1 (executor.hpp:384-408) on the committed buffer after load: x ghosts of
-// own rows, y ghost rows where this rank owns a domain edge.
-__global__ void ghost_fill_rows_kernel(double* b, int P, int R, int nx, int nloc, int j0, int ny,
-                                       SweBC w, SweBC e, SweBC s, SweBC n, const double* z_w,
-                                       const double* z_e, const double* z_s, const double* z_n,
-                                       double h_min) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t < nloc) {
-        const int lr = t;
-        CellVec u0 = {b[pidx(P, R, lr, 0, 0)], b[pidx(P, R, lr, 1, 0)], b[pidx(P, R, lr, 2, 0)]};
-        CellVec g = swe_dev::edge_ghost(SWE_EDGE_W, w, u0, z_w[lr + R], h_min);
-        b[pidx(P, R, lr, 0, -1)] = g.h;
-        b[pidx(P, R, lr, 1, -1)] = g.qx;
-        b[pidx(P, R, lr, 2, -1)] = g.qy;
-        CellVec u1 = {b[pidx(P, R, lr, 0, nx - 1)], b[pidx(P, R, lr, 1, nx - 1)],
-                      b[pidx(P, R, lr, 2, nx - 1)]};
-        g = swe_dev::edge_ghost(SWE_EDGE_E, e, u1, z_e[lr + R], h_min);
-        b[pidx(P, R, lr, 0, nx)] = g.h;
-        b[pidx(P, R, lr, 1, nx)] = g.qx;
-        b[pidx(P, R, lr, 2, nx)] = g.qy;
-    }
-    if (t < nx) {
-        const int i = t;
-        if (j0 == 0) {
-            CellVec u = {b[pidx(P, R, 0, 0, i)], b[pidx(P, R, 0, 1, i)], b[pidx(P, R, 0, 2, i)]};
-            CellVec g = swe_dev::edge_ghost(SWE_EDGE_S, s, u, z_s[i], h_min);
-            b[pidx(P, R, -1, 0, i)] = g.h;
-            b[pidx(P, R, -1, 1, i)] = g.qx;
-            b[pidx(P, R, -1, 2, i)] = g.qy;
-        }
-        if (j0 + nloc == ny) {
-            const int lr = nloc - 1;
-            CellVec u = {b[pidx(P, R, lr, 0, i)], b[pidx(P, R, lr, 1, i)], b[pidx(P, R, lr, 2, i)]};
-            CellVec g = swe_dev::edge_ghost(SWE_EDGE_N, n, u, z_n[i], h_min);
-            b[pidx(P, R, lr + 1, 0, i)] = g.h;
-            b[pidx(P, R, lr + 1, 1, i)] = g.qx;
-            b[pidx(P, R, lr + 1, 2, i)] = g.qy;
-        }
-    }
-}
+}  // namespace swe_rt
 
-// make_domain_ctx slopes (executor.hpp:351-376) for local rows [-R, nloc+R)
-// that lie inside the domain; zp holds z for local rows [-R-1, nloc+R+1)
-// (compact, nx per row; rows outside the domain unused).  Output rows use the
-// padded 2-field layout.  flags[0] |= 1 when any slope bit pattern is not +0.0.
-__global__ void slopes_kernel(const double* zp, double* slope, int P, int R, int nx, int nloc,
-                              int j0, int ny, double two_dx, double two_dy, unsigned* flags) {
-    const int rows = nloc + 2 * R;
-    const size_t n = static_cast<size_t>(rows) * nx;
-    for (size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; k < n;
-         k += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const int lr = static_cast<int>(k / nx) - R;
-        const int i = static_cast<int>(k % nx);
-        const int j = j0 + lr;
-        double sx = 0.0, sy = 0.0;
-        if (j >= 0 && j < ny) {
-            auto zat = [&](int ii, int jj) {
-                return zp[static_cast<size_t>(jj - j0 + R + 1) * nx + ii];
-            };
-            const int iw = max(i - 1, 0), ie = min(i + 1, nx - 1);
-            const int js = max(j - 1, 0), jn = min(j + 1, ny - 1);
-            sx = (zat(ie, j) - zat(iw, j)) / two_dx;
-            sy = (zat(i, jn) - zat(i, js)) / two_dy;
-            if (swe_dev::dbits(sx) != 0ull || swe_dev::dbits(sy) != 0ull) atomicOr(flags, 1u);
-            if (swe_dev::dbits(sy) != 0ull) atomicOr(flags + 2, 1u);
-        }
-        slope[(static_cast<size_t>(lr + R) * 2 + 0) * P + (i + R)] = sx;
-        slope[(static_cast<size_t>(lr + R) * 2 + 1) * P + (i + R)] = sy;
-    }
-}
-
-// Early exit, static part: an item (32-column window x row chunk, the step
-// kernel's unit of work) is eligible when its dependency region -- its cells
-// widened by R + 1 <= 3 -- lies inside this rank's own rows and the domain's
-// columns (no ghost or strip-halo cell involved) and the bed slopes of the 3x3
-// block of items around it are all +0.0 (a flat bed, so the rest state
-// (H, +0, +0) is a fixed point of the step).
-__global__ void item_flat_kernel(const double* slope, int P, int R, int nx, int nloc, int TW, int chunk,
-                                 int ntiles, int nitems, unsigned char* flat) {
-    for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
-        const int rc = item / ntiles, tile = item % ntiles;
-        const int x0 = tile * TW, x1 = min(x0 + TW, nx), y0 = rc * chunk, y1 = min(y0 + chunk, nloc);
-        const int w = x1 - x0;
-        int bad = 0;
-        for (int k = threadIdx.x; k < (y1 - y0) * w; k += blockDim.x) {
-            const int lr = y0 + k / w, i = x0 + k % w;
-            const size_t o = (static_cast<size_t>(lr + R) * 2) * P + (i + R);
-            bad |= (swe_dev::dbits(slope[o]) | swe_dev::dbits(slope[o + P])) != 0ull;
-        }
-        bad = __syncthreads_or(bad);
-        if (threadIdx.x == 0) flat[item] = bad ? 0 : 1;
-    }
-}
-
-__global__ void item_elig_kernel(const unsigned char* flat, int nx, int nloc, int TW, int chunk, int ntiles,
-                                 int nchunks, int R, unsigned char* elig, unsigned long long* count) {
-    const int nitems = ntiles * nchunks;
-    for (int item = blockIdx.x * blockDim.x + threadIdx.x; item < nitems; item += gridDim.x * blockDim.x) {
-        const int rc = item / ntiles, tile = item % ntiles;
-        const int x0 = tile * TW, x1 = min(x0 + TW, nx), y0 = rc * chunk, y1 = min(y0 + chunk, nloc);
-        const int rad = R + 1;
-        bool ok = x0 - rad >= 0 && x1 + rad <= nx && y0 - rad >= 0 && y1 + rad <= nloc && tile >= 1 &&
-                  tile + 1 < ntiles && rc >= 1 && rc + 1 < nchunks && chunk >= rad && TW >= rad;
-        for (int d = 0; ok && d < 9; ++d) ok = flat[(rc + d / 3 - 1) * ntiles + tile + d % 3 - 1] != 0;
-        elig[item] = ok ? 1 : 0;
-        if (ok) atomicAdd(count, 1ull);
-    }
-}
-
-// Bed edge values for the K1 ghosts: z_w / z_e of own rows (local rows
-// [0, nloc) at offset R), from the compact bed rows zp (row lr at lr + R + 1).
-__global__ void edge_z_kernel(const double* zp, int R, int nx, int nloc, double* zw, double* ze) {
-    for (int lr = blockIdx.x * blockDim.x + threadIdx.x; lr < nloc; lr += gridDim.x * blockDim.x) {
-        const double* row = zp + static_cast<size_t>(lr + R + 1) * nx;
-        zw[lr + R] = row[0];
-        ze[lr + R] = row[nx - 1];
-    }
-}
-
-struct BcSet {
-    SweBC bc[4];  // N, S, E, W
-};
-
-// Fixed-elevation clamp diagnostic (grid.hpp:256-263): any fixed-eta edge
-// cell of this rank whose ghost depth eta - z falls below h_min.
-__global__ void clamp_kernel(const double* zp, int R, int nx, int nloc, int own_s, int own_n, BcSet b,
-                             double h_min, unsigned* flag) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    int hit = 0;
-    if (t < nloc) {
-        const double* row = zp + static_cast<size_t>(t + R + 1) * nx;
-        if (b.bc[SWE_EDGE_W].type == SWE_BC_FIXED_ETA && b.bc[SWE_EDGE_W].eta_out - row[0] < h_min) hit = 1;
-        if (b.bc[SWE_EDGE_E].type == SWE_BC_FIXED_ETA && b.bc[SWE_EDGE_E].eta_out - row[nx - 1] < h_min) hit = 1;
-    }
-    if (t < nx) {
-        if (own_s && b.bc[SWE_EDGE_S].type == SWE_BC_FIXED_ETA &&
-            b.bc[SWE_EDGE_S].eta_out - zp[static_cast<size_t>(R + 1) * nx + t] < h_min)
-            hit = 1;
-        if (own_n && b.bc[SWE_EDGE_N].type == SWE_BC_FIXED_ETA &&
-            b.bc[SWE_EDGE_N].eta_out - zp[static_cast<size_t>(R + nloc) * nx + t] < h_min)
-            hit = 1;
-    }
-    if (hit) atomicOr(flag, 1u);
-}
-
-// build_initial_state (scenarios.hpp:95-171) on the device for the kinds
-// without transcendental functions: flat_pool, channel_slope, dam_break.
-// Same expression trees (the TU is compiled -fmad=false), so the state is
-// bit-identical to the reference's; own rows only (strip-local).
-__global__ void initial_kernel(swe_initial ic, double dx, int nx, int nloc, int P, int R, double* buf, double* zp) {
-    const size_t n = static_cast<size_t>(nloc) * nx;
-    for (size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; k < n;
-         k += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const int lr = static_cast<int>(k / nx), i = static_cast<int>(k % nx);
-        double z = 0.0, h = ic.depth;
-        if (ic.kind == SWE_IC_CHANNEL_SLOPE) {
-            z = ic.slope * dx * static_cast<double>(nx - 1 - i);
-            h = ic.depth - z;
-        } else if (ic.kind == SWE_IC_DAM_BREAK) {
-            const double x = (i + 0.5) * dx;
-            h = (x < ic.split_x) ? ic.h_left : ic.h_right;
-        }
-        buf[pidx(P, R, lr, 0, i)] = h;
-        buf[pidx(P, R, lr, 1, i)] = 0.0;
-        buf[pidx(P, R, lr, 2, i)] = 0.0;
-        zp[static_cast<size_t>(lr + R + 1) * nx + i] = z;
-    }
-}
-
-// Scan words (max-combined, like the step reduction).
-enum { SCAN_BAD = 0, SCAN_MINR = 1, SCAN_GUARD = 2, SCAN_N = 4 };
-
-// K6 exact per-cell scan (timestep.hpp:83-105 / executor.hpp:560-580) and K5
-// guard (timestep.hpp:64-78) over own rows of buffer b.
-__global__ void scan_kernel(const double* b, int P, int R, int nx, int nloc, int j0, double g,
-                            double dx, double dy, double h_min, unsigned long long* out) {
-    const size_t n = static_cast<size_t>(nloc) * nx;
-    unsigned long long bad = 0, minr = 0, guard = 0;
-    for (size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; k < n;
-         k += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const int lr = static_cast<int>(k / nx), i = static_cast<int>(k % nx);
-        const double h = b[pidx(P, R, lr, 0, i)], qx = b[pidx(P, R, lr, 1, i)],
-                     qy = b[pidx(P, R, lr, 2, i)];
-        const unsigned long long idx = static_cast<unsigned long long>(j0 + lr) * nx + i;
-        const bool ok = swe_dev::finite_d(h) && swe_dev::finite_d(qx) && swe_dev::finite_d(qy) &&
-                        h >= h_min;
-        if (!ok) guard = max(guard, ~idx);
-        const double c = __dsqrt_rn(g * h);
-        const double sx = fabs(__ddiv_rn(qx, h)) + c;
-        const double sy = fabs(__ddiv_rn(qy, h)) + c;
-        const double r = swe_dev::std_min(__ddiv_rn(dx, sx), __ddiv_rn(dy, sy));
-        if (!(r > 0.0) || !swe_dev::finite_d(r)) {
-            bad = max(bad, ~idx);
-            continue;
-        }
-        minr = max(minr, ~swe_dev::dbits(r));
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-        bad = max(bad, __shfl_xor_sync(0xffffffffu, bad, o));
-        minr = max(minr, __shfl_xor_sync(0xffffffffu, minr, o));
-        guard = max(guard, __shfl_xor_sync(0xffffffffu, guard, o));
-    }
-    if ((threadIdx.x & 31) == 0) {
-        if (bad) atomicMax(&out[SCAN_BAD], bad);
-        if (minr) atomicMax(&out[SCAN_MINR], minr);
-        if (guard) atomicMax(&out[SCAN_GUARD], guard);
-    }
-}
+namespace swe_rt {
 
 // ---------------------------------------------------------------- TMA descriptors
-PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
-// 2D map over field_rows rows of P doubles at row_stride doubles (P if 0); box
-// box_cols x box_rows
 bool encode_rows(CUtensorMap* map, double* base, int P, long long field_rows, int box_rows, std::string& err,
-                 int box_cols = 32, int row_stride = 0) {
+                 int box_cols, int row_stride) {
     if (!g_encode) {
         cudaDriverEntryPointQueryResult q;
         void* fn = nullptr;
@@ -332,19 +77,9 @@ bool encode_rows(CUtensorMap* map, double* base, int P, long long field_rows, in
     return true;
 }
 
-// Shared-reciprocal division of the step kernels (swe_device.cuh), exposed for
-// the parity self-test.  Compiled with -fmad=false like the exact kernels.
-__global__ void selftest_div_kernel(const double* a, const double* b, size_t n, int exact, double* out) {
-    for (size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; k < n;
-         k += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        if (exact) {
-            const swe_dev::Recip rc = swe_dev::make_recip(b[k]);
-            out[k] = swe_dev::div_rn(a[k], rc);
-        } else {
-            out[k] = a[k] * swe_dev::make_recip_fast(b[k]).y;
-        }
-    }
-}
+}  // namespace swe_rt
+
+namespace {
 
 // ---------------------------------------------------------------- helpers
 double std_min(double a, double b) { return (b < a) ? b : a; }
@@ -403,99 +138,8 @@ std::vector<std::pair<int, int>> partition_scanlines(int ny, int workers) {
 
 }  // namespace
 
-// ---------------------------------------------------------------- context
-namespace {
-struct Transport;
-}
-struct swe_ctx {
-    swe_grid g{};
-    swe_physics ph{};
-    swe_policy pol{};
-    swe_boundary_set bnd{};
-    swe_exec ex{};
-    int R = 1, nloc = 0, j0 = 0, pitch = 0, ntiles = 0;
-    bool smooth = false, manning = false, flat = true, xonly = false, loaded = false, exact = true;
-    int clamp_any = 0;
-    int warnings_total = 0;
-    double t = 0.0;
-    int sel = 0;
-    size_t buf_doubles = 0;
-    double* d_buf[2] = {nullptr, nullptr};
-    double* d_slope = nullptr;
-    double *d_zw = nullptr, *d_ze = nullptr, *d_zs = nullptr, *d_zn = nullptr;
-    unsigned long long* d_scan = nullptr;
-    unsigned* d_flags = nullptr;
-    // early exit: quiet flags per buffer, eligibility, per-item flat bits,
-    // counters {skipped cells, eligible items}
-    unsigned long long* d_qflag = nullptr;
-    unsigned char* d_elig = nullptr;
-    unsigned* d_active = nullptr;
-    unsigned char* d_iflat = nullptr;
-    unsigned long long* d_stats = nullptr;
-    int nitems_alloc = 0;
-    bool early = false;
-    SweCtl* d_ctl = nullptr;
-    SweCtl* h_ctl = nullptr;  // pinned mirror
-    double* d_zp = nullptr;  // bed rows [-R-1, nloc+R+1) (compact, nx per row, strip halos): state() z, slopes
-    cudaStream_t stream = nullptr;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    StepParams prm{};
-    int ncta = 0;
-    int occ = 1;
-    cudaGraphExec_t graph[2] = {nullptr, nullptr};
-    int graph_len = 0;
-    unsigned long long graph_kernels = 0;  // our kernels in one captured graph
-    Transport* tr = nullptr;  // row-strip collectives (NCCL or local group); null for one rank
-    unsigned long long* d_xr = nullptr;  // local-group allreduce scratch
-    // strips: halo exchange overlapped with the interior (edge + interior launches)
-    bool overlap = false;
-    StepParams prm_edge{}, prm_int{};
-    int ncta_edge = 0;
-    cudaStream_t stream_edge = nullptr;
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-    unsigned long long launches = 0;
-    swe_timing timing{};
-    double tz_x = 0, tz_y = 0;
-    int always_diag = 0;
-};
-
 namespace {
 
-int set_status(swe_status* st, int code, int i, int j, double t, const char* fmt, ...) {
-    if (st) {
-        std::memset(st, 0, sizeof *st);
-        st->code = code;
-        st->i = i;
-        st->j = j;
-        st->t = t;
-        va_list ap;
-        va_start(ap, fmt);
-        std::vsnprintf(st->msg, sizeof st->msg, fmt, ap);
-        va_end(ap);
-    }
-    return code;
-}
-
-int ok_status(swe_status* st) {
-    if (st) std::memset(st, 0, sizeof *st);
-    return SWE_OK;
-}
-
-#define CUDA_TRY(x)                                                                              \
-    do {                                                                                         \
-        cudaError_t e_ = (x);                                                                    \
-        if (e_ != cudaSuccess)                                                                   \
-            return set_status(st, SWE_ERR_RUNTIME, -1, -1, 0.0, "CUDA error %s at %s:%d",        \
-                              cudaGetErrorString(e_), __FILE__, __LINE__);                       \
-    } while (0)
-
-#define NCCL_TRY(x)                                                                              \
-    do {                                                                                         \
-        ncclResult_t r_ = (x);                                                                   \
-        if (r_ != ncclSuccess)                                                                   \
-            return set_status(st, SWE_ERR_RUNTIME, -1, -1, 0.0, "NCCL error %d at %s:%d",        \
-                              static_cast<int>(r_), __FILE__, __LINE__);                         \
-    } while (0)
 
 bool is_fin(double x) { return std::isfinite(x); }
 
@@ -544,175 +188,9 @@ int validate(const swe_grid* g, const swe_physics* p, const swe_policy* pol,
     return SWE_OK;
 }
 
-// ---------------------------------------------------------------- strip transport
-// The row-strip protocol needs two collectives: an
-// unsigned-max allreduce of the reduction words (error indices are stored
-// complemented, so max = row-major first offender; non-negative doubles order
-// like their bit patterns) and a send/recv of R halo rows with each strip
-// neighbour.  Between GPUs NCCL carries them over NVLink.  The local group
-// carries them between contexts of one process on one device (one host thread
-// per rank, ordered by CUDA events, no kernel ever waits on another rank's):
-// it lets the GPU tests check the whole strip path bit for bit on one B200.
-struct Transport {
-    virtual ~Transport() = default;
-    virtual int allreduce_max(swe_ctx* c, cudaStream_t s, unsigned long long* d, int n, swe_status* st) = 0;
-    // send_up -> (rank+1).recv_down, send_down -> (rank-1).recv_up, `bytes` each;
-    // null pointers where the neighbour does not exist
-    virtual int sendrecv(swe_ctx* c, cudaStream_t s, const void* send_up, void* recv_up, const void* send_down,
-                         void* recv_down, size_t bytes, swe_status* st) = 0;
-    virtual bool capturable() const = 0;  // may be recorded into a CUDA graph
-};
-
-struct NcclTransport final : Transport {
-    ncclComm_t comm = nullptr;
-    ~NcclTransport() override {
-        if (comm && g_nccl.CommDestroy) g_nccl.CommDestroy(comm);
-    }
-    int allreduce_max(swe_ctx* c, cudaStream_t s, unsigned long long* d, int n, swe_status* st) override;
-    int sendrecv(swe_ctx* c, cudaStream_t s, const void* su, void* ru, const void* sd, void* rd, size_t bytes,
-                 swe_status* st) override;
-    bool capturable() const override { return true; }
-};
-
-constexpr int kMaxLocalRanks = 16;
-struct RedPtrs {
-    const unsigned long long* p[kMaxLocalRanks];
-};
-__global__ void max_reduce_kernel(RedPtrs in, int nranks, int n, unsigned long long* out) {
-    const int k = threadIdx.x;
-    if (k >= n) return;
-    unsigned long long m = 0ull;
-    for (int r = 0; r < nranks; ++r) m = max(m, in.p[r][k]);
-    out[k] = m;
-}
-
-struct LocalGroup {
-    std::mutex m;
-    std::condition_variable cv;
-    int n = 0, arrived = 0, refs = 0;
-    unsigned long long gen = 0;
-    bool broken = false;
-    cudaEvent_t ready[kMaxLocalRanks] = {}, done[kMaxLocalRanks] = {};
-    const void* su[kMaxLocalRanks] = {};
-    const void* sd[kMaxLocalRanks] = {};
-    const unsigned long long* red[kMaxLocalRanks] = {};
-    // all ranks arrive (or a 120 s timeout breaks the group, so a failing
-    // test cannot hang the box)
-    bool barrier() {
-        std::unique_lock<std::mutex> lk(m);
-        if (broken) return false;
-        const unsigned long long g = gen;
-        if (++arrived == n) {
-            arrived = 0;
-            ++gen;
-            cv.notify_all();
-            return true;
-        }
-        if (!cv.wait_for(lk, std::chrono::seconds(120), [&] { return gen != g || broken; })) broken = true;
-        if (broken) {
-            cv.notify_all();
-            return false;
-        }
-        return true;
-    }
-};
-std::mutex g_groups_m;
-std::map<std::string, LocalGroup*> g_groups;
-
-struct LocalTransport final : Transport {
-    LocalGroup* grp = nullptr;
-    std::string key;
-    int rank = 0;
-    ~LocalTransport() override {
-        std::lock_guard<std::mutex> lk(g_groups_m);
-        if (grp && --grp->refs == 0) {
-            for (int r = 0; r < grp->n; ++r) {
-                if (grp->ready[r]) cudaEventDestroy(grp->ready[r]);
-                if (grp->done[r]) cudaEventDestroy(grp->done[r]);
-            }
-            g_groups.erase(key);
-            delete grp;
-        }
-    }
-    int allreduce_max(swe_ctx* c, cudaStream_t s, unsigned long long* d, int n, swe_status* st) override;
-    int sendrecv(swe_ctx* c, cudaStream_t s, const void* su, void* ru, const void* sd, void* rd, size_t bytes,
-                 swe_status* st) override;
-    bool capturable() const override { return false; }
-};
-
 double* row_ptr(swe_ctx* c, int which, int lr) {
     return c->d_buf[which] + static_cast<size_t>(lr + c->R) * 3 * c->pitch;
 }
-
-int NcclTransport::allreduce_max(swe_ctx* c, cudaStream_t s, unsigned long long* d, int n, swe_status* st) {
-    (void)c;
-    NCCL_TRY(g_nccl.AllReduce(d, d, static_cast<size_t>(n), ncclUint64, ncclMax, comm, s));
-    return SWE_OK;
-}
-
-int NcclTransport::sendrecv(swe_ctx* c, cudaStream_t s, const void* su, void* ru, const void* sd, void* rd,
-                            size_t bytes, swe_status* st) {
-    const int rk = c->ex.rank;
-    NCCL_TRY(g_nccl.GroupStart());
-    if (su) NCCL_TRY(g_nccl.Send(su, bytes, ncclUint8, rk + 1, comm, s));
-    if (ru) NCCL_TRY(g_nccl.Recv(ru, bytes, ncclUint8, rk + 1, comm, s));
-    if (sd) NCCL_TRY(g_nccl.Send(sd, bytes, ncclUint8, rk - 1, comm, s));
-    if (rd) NCCL_TRY(g_nccl.Recv(rd, bytes, ncclUint8, rk - 1, comm, s));
-    NCCL_TRY(g_nccl.GroupEnd());
-    return SWE_OK;
-}
-
-#define GROUP_SYNC()                                                                                   \
-    do {                                                                                               \
-        if (!grp->barrier())                                                                           \
-            return set_status(st, SWE_ERR_RUNTIME, -1, -1, 0.0, "local strip group: a rank timed out"); \
-    } while (0)
-
-// post -> barrier -> read the neighbours' posts -> barrier -> wait for the
-// neighbours' reads before the posted rows may change again
-int LocalTransport::sendrecv(swe_ctx* c, cudaStream_t s, const void* su, void* ru, const void* sd, void* rd,
-                             size_t bytes, swe_status* st) {
-    (void)c;
-    const int r = rank, n = grp->n;
-    grp->su[r] = su;
-    grp->sd[r] = sd;
-    CUDA_TRY(cudaEventRecord(grp->ready[r], s));
-    GROUP_SYNC();
-    if (ru && r + 1 < n) {
-        CUDA_TRY(cudaStreamWaitEvent(s, grp->ready[r + 1], 0));
-        CUDA_TRY(cudaMemcpyAsync(ru, grp->sd[r + 1], bytes, cudaMemcpyDeviceToDevice, s));
-    }
-    if (rd && r > 0) {
-        CUDA_TRY(cudaStreamWaitEvent(s, grp->ready[r - 1], 0));
-        CUDA_TRY(cudaMemcpyAsync(rd, grp->su[r - 1], bytes, cudaMemcpyDeviceToDevice, s));
-    }
-    CUDA_TRY(cudaEventRecord(grp->done[r], s));
-    GROUP_SYNC();
-    if (r + 1 < n) CUDA_TRY(cudaStreamWaitEvent(s, grp->done[r + 1], 0));
-    if (r > 0) CUDA_TRY(cudaStreamWaitEvent(s, grp->done[r - 1], 0));
-    return SWE_OK;
-}
-
-int LocalTransport::allreduce_max(swe_ctx* c, cudaStream_t s, unsigned long long* d, int n, swe_status* st) {
-    const int r = rank, nr = grp->n;
-    grp->red[r] = d;
-    CUDA_TRY(cudaEventRecord(grp->ready[r], s));
-    GROUP_SYNC();
-    RedPtrs in{};
-    for (int k = 0; k < nr; ++k) {
-        CUDA_TRY(cudaStreamWaitEvent(s, grp->ready[k], 0));
-        in.p[k] = grp->red[k];
-    }
-    max_reduce_kernel<<<1, 32, 0, s>>>(in, nr, n, c->d_xr);
-    CUDA_TRY(cudaGetLastError());
-    CUDA_TRY(cudaEventRecord(grp->done[r], s));
-    GROUP_SYNC();
-    for (int k = 0; k < nr; ++k) CUDA_TRY(cudaStreamWaitEvent(s, grp->done[k], 0));
-    CUDA_TRY(cudaMemcpyAsync(d, c->d_xr, static_cast<size_t>(n) * sizeof(unsigned long long),
-                             cudaMemcpyDeviceToDevice, s));
-    return SWE_OK;
-}
-#undef GROUP_SYNC
 
 // Exchange R committed rows with the strip neighbours:
 // own top rows -> rank+1's lower halo, own bottom rows -> rank-1's upper halo.
@@ -928,14 +406,7 @@ int build_graphs(swe_ctx* c, int len, swe_status* st) {
 
 EXPORT const char* swe_cuda_version(void) { return "swe-b200 1.0 (sm_100a, ABI 1)"; }
 
-EXPORT int swe_cuda_nccl_unique_id(void* out, swe_status* st) {
-    std::string err;
-    if (!g_nccl.load(err)) return set_status(st, SWE_ERR_RUNTIME, -1, -1, 0, "%s", err.c_str());
-    ncclUniqueId id;
-    NCCL_TRY(g_nccl.GetUniqueId(&id));
-    std::memcpy(out, &id, sizeof id);
-    return ok_status(st);
-}
+EXPORT int swe_cuda_nccl_unique_id(void* out, swe_status* st) { return nccl_unique_id(out, st); }
 
 EXPORT int swe_cuda_create(const swe_grid* grid, const swe_physics* phys, const swe_policy* pol,
                            const swe_boundary_set* bnd, const swe_exec* exec, swe_ctx** out,
@@ -1021,35 +492,8 @@ EXPORT int swe_cuda_create(const swe_grid* grid, const swe_physics* phys, const 
         if (!exec->nccl_id)
             return set_status(st, SWE_ERR_CONFIG, -1, -1, 0, "exec: nranks > 1 requires nccl_id");
         CUDA_TRY(cudaMalloc(&c->d_xr, 16 * sizeof(unsigned long long)));
-        if (ex.flags & SWE_EXEC_LOCAL_GROUP) {
-            if (ex.nranks > kMaxLocalRanks)
-                return set_status(st, SWE_ERR_CONFIG, -1, -1, 0, "exec: a local group holds at most %d ranks",
-                                  kMaxLocalRanks);
-            auto* t = new LocalTransport();
-            c->tr = t;
-            t->key.assign(static_cast<const char*>(exec->nccl_id), SWE_NCCL_ID_BYTES);
-            t->rank = ex.rank;
-            std::lock_guard<std::mutex> lk(g_groups_m);
-            LocalGroup*& g = g_groups[t->key];
-            if (!g) {
-                g = new LocalGroup();
-                g->n = ex.nranks;
-            }
-            if (g->n != ex.nranks)
-                return set_status(st, SWE_ERR_CONFIG, -1, -1, 0, "exec: local group size mismatch");
-            ++g->refs;
-            t->grp = g;
-            CUDA_TRY(cudaEventCreateWithFlags(&g->ready[ex.rank], cudaEventDisableTiming));
-            CUDA_TRY(cudaEventCreateWithFlags(&g->done[ex.rank], cudaEventDisableTiming));
-        } else {
-            std::string err;
-            if (!g_nccl.load(err)) return set_status(st, SWE_ERR_RUNTIME, -1, -1, 0, "%s", err.c_str());
-            auto* t = new NcclTransport();
-            c->tr = t;
-            ncclUniqueId id;
-            std::memcpy(&id, exec->nccl_id, sizeof id);
-            NCCL_TRY(g_nccl.CommInitRank(&t->comm, ex.nranks, id, ex.rank));
-        }
+        const int trc = create_transport(c, ex, exec->nccl_id, st);
+        if (trc) return trc;
     }
 
     // K6 diagnosis thresholds (see swe_step.cuh finalize_step)
