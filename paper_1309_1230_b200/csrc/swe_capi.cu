@@ -532,6 +532,7 @@ EXPORT int swe_cuda_create(const swe_grid* grid, const swe_physics* phys, const 
     p.dy = grid->dy;
     p.g = phys->g;
     p.half_g = 0.5 * phys->g;
+    p.sqrt_g = std::sqrt(phys->g);
     p.neg_g = -phys->g;
     p.gnn = phys->g * phys->manning_n * phys->manning_n;
     p.h_min = pol->h_min;

@@ -385,10 +385,17 @@ struct Marcher {
     template <bool EDGE>
     __device__ __forceinline__ void emit(const CellVec& o, int rr) {
         const int jj = p.j0 + rr;
-        const Rc rc = A::recip(o.h);  // executor.hpp:560-580
-        const double c = A::sqrt_(p.g * o.h);
-        double u, v;
-        A::div2(o.qx, o.qy, rc, u, v);
+        double u, v, c;  // executor.hpp:560-580
+        if constexpr (EXACT) {
+            const Rc rc = A::recip(o.h);
+            c = A::sqrt_(p.g * o.h);
+            A::div2(o.qx, o.qy, rc, u, v);
+        } else {
+            double rh;
+            cfl_fast(o.h, p.sqrt_g, rh, c);
+            u = o.qx * rh;
+            v = o.qy * rh;
+        }
         const double sx = fabs(u) + c, sy = fabs(v) + c;
         // guard (executor.hpp:543-558): a non-finite h, qx or qy always makes
         // sx + sy non-finite, so one test screens the cell; the exact test
@@ -556,7 +563,7 @@ struct Marcher {
             consume<GI>(out.U, out.zx, out.zy);
             const Rc rcN = A::recip(out.U.h);
             out.FU = A::flux(out.U, rcN, half_g);
-            source_of<EXACT, MANNING>(out.U, out.FU, rcN, out.zx, out.zy, neg_g, gnn, out.srx, out.sry);
+            source_of<EXACT, MANNING, FLAT, FLAT || XONLY>(out.U, out.FU, rcN, out.zx, out.zy, neg_g, gnn, out.srx, out.sry);
 
             // ======== stage 2: predictor at (i, b)   scheme.hpp:100-113
             const CellVec& U = in.U;
@@ -604,7 +611,7 @@ struct Marcher {
             const Rc rcS = A::recip(Us.h);
             const Flux FS = A::flux(Us, rcS, half_g);
             double ssx, ssy;
-            source_of<EXACT, MANNING>(Us, FS, rcS, in.zx, in.zy, neg_g, gnn, ssx, ssy);
+            source_of<EXACT, MANNING, FLAT, FLAT || XONLY>(Us, FS, rcS, in.zx, in.zy, neg_g, gnn, ssx, ssy);
 
             // own x face (FWD: east, BWD: west) and y face (b, b+S)   scheme.hpp:153-161
             CellVec Hx = {avg(fn_h, Us.qx), avg(fn_qx, FS.fxx), avg(fn_qy, FS.fxy)};
@@ -732,7 +739,7 @@ struct Marcher {
         {
             const Rc rc = A::recip(A.U.h);
             A.FU = A::flux(A.U, rc, half_g);
-            source_of<EXACT, MANNING>(A.U, A.FU, rc, A.zx, A.zy, neg_g, gnn, A.srx, A.sry);
+            source_of<EXACT, MANNING, FLAT, FLAT || XONLY>(A.U, A.FU, rc, A.zx, A.zy, neg_g, gnn, A.srx, A.sry);
         }
         A.Hyp = {0.0, 0.0, 0.0};
         A.Cp = {0.0, 0.0, 0.0};
@@ -949,7 +956,14 @@ __global__ void __launch_bounds__(256) swe_schedule_kernel(const __grid_constant
             for (int d = 0; skip && d < 9; ++d)
                 skip = p.qflag[sel][(rc + d / 3 - 1) * p.ntiles + tile + d % 3 - 1] == c;
             if (skip) {
-                const double s = Arith<EXACT>::sqrt_(p.g * __longlong_as_double(static_cast<long long>(c)));
+                const double H = __longlong_as_double(static_cast<long long>(c));
+                double s;  // the epilogue's own arithmetic for sqrt(g H)
+                if constexpr (EXACT) {
+                    s = Arith<EXACT>::sqrt_(p.g * H);
+                } else {
+                    double rh;
+                    cfl_fast(H, p.sqrt_g, rh, s);
+                }
                 smax = (s > smax) ? s : smax;
                 const int ra = rc * p.chunk, rb = min(ra + p.chunk, p.nloc);
                 const int x0 = tile * tw, x1 = min(x0 + tw, p.nx);

@@ -101,6 +101,7 @@ struct StepParams {
     int finalize;          // 1: last CTA finalizes (one rank); 0: host-side allreduce + finalize kernel
     int nranks;
     double dx, dy, g, half_g, neg_g, gnn, h_min, nu;
+    double sqrt_g;         // fast-mode CFL speed sqrt(g) * h^(1/2)
     double cfl, dt_max, dt_min;
     double tz_x, tz_y;     // K6 diagnosis triggers (dx/sx would round to 0)
     int always_diag;       // pathological parameters: diagnose every step
