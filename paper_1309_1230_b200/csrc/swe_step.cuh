@@ -687,9 +687,15 @@ struct Marcher {
                         }
                         const double nu = p.nu;
                         CellVec o;
-                        o.h = Cp.h + nu * (((ce.h - Cp.h) + (cw.h - Cp.h)) + ((cn.h - Cp.h) + (cs.h - Cp.h)));
-                        o.qx = Cp.qx + nu * (((ce.qx - Cp.qx) + (cw.qx - Cp.qx)) + ((cn.qx - Cp.qx) + (cs.qx - Cp.qx)));
-                        o.qy = Cp.qy + nu * (((ce.qy - Cp.qy) + (cw.qy - Cp.qy)) + ((cn.qy - Cp.qy) + (cs.qy - Cp.qy)));
+                        if constexpr (EXACT) {
+                            o.h = Cp.h + nu * (((ce.h - Cp.h) + (cw.h - Cp.h)) + ((cn.h - Cp.h) + (cs.h - Cp.h)));
+                            o.qx = Cp.qx + nu * (((ce.qx - Cp.qx) + (cw.qx - Cp.qx)) + ((cn.qx - Cp.qx) + (cs.qx - Cp.qx)));
+                            o.qy = Cp.qy + nu * (((ce.qy - Cp.qy) + (cw.qy - Cp.qy)) + ((cn.qy - Cp.qy) + (cs.qy - Cp.qy)));
+                        } else {  // U + nu (E + W + N + S - 4U), contracted
+                            o.h = __fma_rn(nu, __fma_rn(-4.0, Cp.h, (ce.h + cw.h) + (cn.h + cs.h)), Cp.h);
+                            o.qx = __fma_rn(nu, __fma_rn(-4.0, Cp.qx, (ce.qx + cw.qx) + (cn.qx + cs.qx)), Cp.qx);
+                            o.qy = __fma_rn(nu, __fma_rn(-4.0, Cp.qy, (ce.qy + cw.qy) + (cn.qy + cs.qy)), Cp.qy);
+                        }
                         emit<EDGE>(o, q);
                     }
                 }
