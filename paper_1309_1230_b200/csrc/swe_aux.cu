@@ -7,6 +7,8 @@
 namespace swe_rt {
 
 using swe_dev::CellVec;
+constexpr int swe_dev_edge_n = SWE_EDGE_N, swe_dev_edge_s = SWE_EDGE_S, swe_dev_edge_e = SWE_EDGE_E,
+              swe_dev_edge_w = SWE_EDGE_W;
 
 __device__ __forceinline__ size_t pidx(int P, int R, int lr, int f, int i) {
     return (static_cast<size_t>(lr + R) * 3 + f) * P + static_cast<size_t>(i + R);
@@ -69,28 +71,48 @@ __global__ void ghost_fill_rows_kernel(double* b, int P, int R, int nx, int nloc
 // (compact, nx per row; rows outside the domain unused).  Output rows use the
 // padded 2-field layout.  flags[0] |= 1 when any slope bit pattern is not +0.0.
 __global__ void slopes_kernel(const double* zp, double* slope, int P, int R, int nx, int nloc,
-                              int j0, int ny, double two_dx, double two_dy, unsigned* flags) {
+                              int j0, int ny, double two_dx, double two_dy, double scale, unsigned* flags) {
+    // one row per block iteration, columns across the threads (coalesced);
+    // the flat / dz/dy flags are OR-ed per warp, then once per block
+    __shared__ unsigned s_any, s_y;
+    if (threadIdx.x == 0) s_any = s_y = 0u;
+    __syncthreads();
+    unsigned any = 0u, anyy = 0u;
     const int rows = nloc + 2 * R;
-    const size_t n = static_cast<size_t>(rows) * nx;
-    for (size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; k < n;
-         k += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const int lr = static_cast<int>(k / nx) - R;
-        const int i = static_cast<int>(k % nx);
+    for (int rr = blockIdx.x; rr < rows; rr += gridDim.x) {
+        const int lr = rr - R;
         const int j = j0 + lr;
-        double sx = 0.0, sy = 0.0;
-        if (j >= 0 && j < ny) {
-            auto zat = [&](int ii, int jj) {
-                return zp[static_cast<size_t>(jj - j0 + R + 1) * nx + ii];
-            };
-            const int iw = max(i - 1, 0), ie = min(i + 1, nx - 1);
-            const int js = max(j - 1, 0), jn = min(j + 1, ny - 1);
-            sx = (zat(ie, j) - zat(iw, j)) / two_dx;
-            sy = (zat(i, jn) - zat(i, js)) / two_dy;
-            if (swe_dev::dbits(sx) != 0ull || swe_dev::dbits(sy) != 0ull) atomicOr(flags, 1u);
-            if (swe_dev::dbits(sy) != 0ull) atomicOr(flags + 2, 1u);
+        const bool own = j >= 0 && j < ny;
+        const double* zr = zp + static_cast<size_t>(lr + R + 1) * nx;  // bed row j
+        const int js = max(j - 1, 0) - j, jn = min(j + 1, ny - 1) - j;    // clamped row offsets
+        double* sxr = slope + (static_cast<size_t>(rr) * 2 + 0) * P + R;
+        double* syr = slope + (static_cast<size_t>(rr) * 2 + 1) * P + R;
+        for (int i = threadIdx.x; i < nx; i += blockDim.x) {
+            double sx = 0.0, sy = 0.0;
+            if (own) {  // make_domain_ctx (executor.hpp:351-376): clamped central differences
+                const int iw = max(i - 1, 0), ie = min(i + 1, nx - 1);
+                sx = (zr[ie] - zr[iw]) / two_dx;
+                sy = (zr[static_cast<ptrdiff_t>(jn) * nx + i] - zr[static_cast<ptrdiff_t>(js) * nx + i]) / two_dy;
+            }
+            const bool nzx = swe_dev::dbits(sx) != 0ull, nzy = swe_dev::dbits(sy) != 0ull;
+            any |= static_cast<unsigned>(nzx || nzy);
+            anyy |= static_cast<unsigned>(nzy);
+            // fast mode stores -g * slope (one FMA for the bed source term);
+            // +0.0 stays +0.0 so flat items are recognised by their bit patterns
+            sxr[i] = nzx ? sx * scale : sx;
+            syr[i] = nzy ? sy * scale : sy;
         }
-        slope[(static_cast<size_t>(lr + R) * 2 + 0) * P + (i + R)] = sx;
-        slope[(static_cast<size_t>(lr + R) * 2 + 1) * P + (i + R)] = sy;
+    }
+    any = __any_sync(0xffffffffu, any);
+    anyy = __any_sync(0xffffffffu, anyy);
+    if ((threadIdx.x & 31) == 0) {
+        if (any) atomicOr(&s_any, 1u);
+        if (anyy) atomicOr(&s_y, 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (s_any) atomicOr(flags, 1u);
+        if (s_y) atomicOr(flags + 2, 1u);
     }
 }
 
@@ -194,26 +216,29 @@ __global__ void initial_kernel(swe_initial ic, double dx, int nx, int nloc, int 
 // guard (timestep.hpp:64-78) over own rows of buffer b.
 __global__ void scan_kernel(const double* b, int P, int R, int nx, int nloc, int j0, double g,
                             double dx, double dy, double h_min, unsigned long long* out) {
-    const size_t n = static_cast<size_t>(nloc) * nx;
+    // one row per block iteration, columns across the threads (coalesced)
     unsigned long long bad = 0, minr = 0, guard = 0;
-    for (size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; k < n;
-         k += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const int lr = static_cast<int>(k / nx), i = static_cast<int>(k % nx);
-        const double h = b[pidx(P, R, lr, 0, i)], qx = b[pidx(P, R, lr, 1, i)],
-                     qy = b[pidx(P, R, lr, 2, i)];
-        const unsigned long long idx = static_cast<unsigned long long>(j0 + lr) * nx + i;
-        const bool ok = swe_dev::finite_d(h) && swe_dev::finite_d(qx) && swe_dev::finite_d(qy) &&
-                        h >= h_min;
-        if (!ok) guard = max(guard, ~idx);
-        const double c = __dsqrt_rn(g * h);
-        const double sx = fabs(__ddiv_rn(qx, h)) + c;
-        const double sy = fabs(__ddiv_rn(qy, h)) + c;
-        const double r = swe_dev::std_min(__ddiv_rn(dx, sx), __ddiv_rn(dy, sy));
-        if (!(r > 0.0) || !swe_dev::finite_d(r)) {
-            bad = max(bad, ~idx);
-            continue;
+    for (int lr = blockIdx.x; lr < nloc; lr += gridDim.x) {
+        const double* hr = b + pidx(P, R, lr, 0, 0);
+        const unsigned long long row0 = static_cast<unsigned long long>(j0 + lr) * nx;
+        for (int i = threadIdx.x; i < nx; i += blockDim.x) {
+            const double h = hr[i], qx = hr[P + i], qy = hr[2 * P + i];
+            const unsigned long long idx = row0 + i;
+            // stability guard (executor.hpp:543-556)
+            const bool ok = swe_dev::finite_d(h) && swe_dev::finite_d(qx) && swe_dev::finite_d(qy) &&
+                            h >= h_min;
+            if (!ok) guard = max(guard, ~idx);
+            // K6 (executor.hpp:560-580)
+            const double c = __dsqrt_rn(g * h);
+            const double sx = fabs(__ddiv_rn(qx, h)) + c;
+            const double sy = fabs(__ddiv_rn(qy, h)) + c;
+            const double r = swe_dev::std_min(__ddiv_rn(dx, sx), __ddiv_rn(dy, sy));
+            if (!(r > 0.0) || !swe_dev::finite_d(r)) {
+                bad = max(bad, ~idx);
+                continue;
+            }
+            minr = max(minr, ~swe_dev::dbits(r));
         }
-        minr = max(minr, ~swe_dev::dbits(r));
     }
     for (int o = 16; o > 0; o >>= 1) {
         bad = max(bad, __shfl_xor_sync(0xffffffffu, bad, o));
@@ -225,6 +250,57 @@ __global__ void scan_kernel(const double* b, int P, int R, int nx, int nloc, int
         if (minr) atomicMax(&out[SCAN_MINR], minr);
         if (guard) atomicMax(&out[SCAN_GUARD], guard);
     }
+}
+
+// K4's dry-U* check (executor.hpp:429-436, 451-513) for every corrector cell
+// of this rank's rows, from the committed buffer: U*.h needs only h of the
+// cell and the momenta of its sweep neighbours (scheme.hpp:100-113), formed
+// with the step kernel's arithmetic for the mode.  Reports the row-major first
+// consumer whose own U* or a neighbour U* its corrector reads is dry (NaN
+// counts as dry).  Run only after a step whose interior windows flagged one.
+__global__ void dry_scan_kernel(const double* b, int P, int R, int nx, int ny, int nloc, int j0, double dt,
+                                double dx, double dy, int fwd, int exact, BcSet bs, const double* z_w,
+                                const double* z_e, const double* z_s, const double* z_n, double h_min,
+                                unsigned long long* out) {
+    const double dtdx = dt / dx, dtdy = dt / dy;
+    const int s = fwd ? 1 : -1;
+    auto star_h = [&](int lr, int i) {  // U*.h of interior cell (i, local row lr)
+        const double h = b[pidx(P, R, lr, 0, i)], qx = b[pidx(P, R, lr, 1, i)], qy = b[pidx(P, R, lr, 2, i)];
+        const double qxn = b[pidx(P, R, lr, 1, i + s)], qyn = b[pidx(P, R, lr + s, 2, i)];
+        const double df = fwd ? qxn - qx : qx - qxn, dg = fwd ? qyn - qy : qy - qyn;
+        if (exact) return (h - (dtdx * df + dtdy * dg)) + 0.0;
+        return h - __fma_rn(dtdx, df, dtdy * dg);
+    };
+    auto wet = [&](double x) { return x >= h_min; };
+    unsigned long long first = 0;
+    for (int lr = blockIdx.x; lr < nloc; lr += gridDim.x) {
+        const int j = j0 + lr;
+        for (int i = threadIdx.x; i < nx; i += blockDim.x) {
+            const double own = star_h(lr, i);
+            bool dry = !wet(own);
+            // faces whose U* is the neighbour's (FWD: west and south; BWD: east
+            // and north); wall and inflow faces read no neighbour U*; an edge
+            // face of another kind reads the U* ghost of this cell
+            auto face = [&](int edge, bool at_edge, int di, int dj) {
+                const SweBC& bc = bs.bc[edge];
+                if (at_edge) {
+                    if (bc.type == SWE_BC_WALL || bc.type == SWE_BC_INFLOW) return true;
+                    const double zin = edge == swe_dev_edge_w ? z_w[lr + R] : edge == swe_dev_edge_e ? z_e[lr + R]
+                                       : edge == swe_dev_edge_s ? z_s[i] : z_n[i];
+                    const CellVec us = {own, 0.0, 0.0};
+                    return wet(swe_dev::edge_ghost(edge, bc, us, zin, h_min).h);
+                }
+                return wet(star_h(lr + dj, i + di));
+            };
+            if (!dry && fwd) dry = !face(swe_dev_edge_w, i == 0, -1, 0);
+            if (!dry && !fwd) dry = !face(swe_dev_edge_e, i == nx - 1, 1, 0);
+            if (!dry && fwd) dry = !face(swe_dev_edge_s, j == 0, 0, -1);
+            if (!dry && !fwd) dry = !face(swe_dev_edge_n, j == ny - 1, 0, 1);
+            if (dry) first = max(first, ~(static_cast<unsigned long long>(j) * nx + i));
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) first = max(first, __shfl_xor_sync(0xffffffffu, first, o));
+    if ((threadIdx.x & 31) == 0 && first) atomicMax(&out[SCAN_DRY], first);
 }
 
 // Shared-reciprocal division of the step kernels (swe_device.cuh), exposed for

@@ -279,6 +279,27 @@ int run_scan(swe_ctx* c, int which, unsigned long long out[SCAN_N], swe_status* 
     return SWE_OK;
 }
 
+// First row-major corrector cell consuming a dry U* (dry_scan_kernel over
+// this rank's rows of the committed buffer), all-reduced; 0 = none.
+int run_dry_scan(swe_ctx* c, double dt, bool fwd, unsigned long long* first, swe_status* st) {
+    CUDA_TRY(cudaMemsetAsync(c->d_scan, 0, SCAN_N * sizeof(unsigned long long), c->stream));
+    BcSet b;
+    for (int e = 0; e < 4; ++e) b.bc[e] = c->prm.bc[e];
+    dry_scan_kernel<<<std::max(1, std::min(c->nloc, 148 * 8)), 256, 0, c->stream>>>(
+        c->d_buf[c->sel], c->pitch, c->R, c->g.nx, c->g.ny, c->nloc, c->j0, dt, c->g.dx, c->g.dy, fwd ? 1 : 0,
+        c->exact ? 1 : 0, b, c->d_zw, c->d_ze, c->d_zs, c->d_zn, c->pol.h_min, c->d_scan);
+    CUDA_TRY(cudaGetLastError());
+    if (c->ex.nranks > 1) {
+        int rc = c->tr->allreduce_max(c, c->stream, c->d_scan, SCAN_N, st);
+        if (rc) return rc;
+    }
+    unsigned long long sc[SCAN_N];
+    CUDA_TRY(cudaMemcpyAsync(sc, c->d_scan, sizeof sc, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    *first = sc[SCAN_DRY];
+    return SWE_OK;
+}
+
 // Values of global cell idx from buffer `which` (the owning rank answers;
 // others return NaN).
 void cell_values(swe_ctx* c, int which, unsigned long long idx, double* h, double* qx, double* qy) {
@@ -295,17 +316,102 @@ void cell_values(swe_ctx* c, int which, unsigned long long idx, double* h, doubl
     *qy = v[2];
 }
 
+// Depth of the dry predicted state that failed the corrector's check at
+// consumer (i, j) (executor.hpp:429-436, 451-513: own U* first, then the
+// west, east, south and north U* the corrector reads).  U*.h only needs
+// h of the cell and the momenta of its sweep neighbours
+// (scheme.hpp:100-113), so the host recomputes it from the intact committed
+// buffer with the kernel's arithmetic.  NaN when a needed row is not held by
+// this rank.
+double dry_star_depth(swe_ctx* c, int i, int j, double dt, bool fwd) {
+    const int nx = c->g.nx, ny = c->g.ny, R = c->R, P = c->pitch;
+    const int lj = j - c->j0;
+    if (lj - 1 < -R || lj + 1 >= c->nloc + R) return std::numeric_limits<double>::quiet_NaN();
+    // rows lj-1 .. lj+1, padded columns i-1 .. i+1 of h, qx, qy
+    double v[3][3][3];  // [row][field][col]
+    for (int r = 0; r < 3; ++r)
+        for (int f = 0; f < 3; ++f)
+            cudaMemcpy(v[r][f], c->d_buf[c->sel] + (static_cast<size_t>(lj - 1 + r + R) * 3 + f) * P + (i - 1 + R),
+                       3 * sizeof(double), cudaMemcpyDeviceToHost);
+    const double dtdx = dt / c->g.dx, dtdy = dt / c->g.dy;
+    const int s = fwd ? 1 : -1;
+    auto star_h = [&](int di, int dj) {  // U*.h of cell (i+di, j+dj), |di|,|dj| <= 1
+        const int r = 1 + dj, col = 1 + di;
+        const double hh = v[r][0][col], qx = v[r][1][col], qy = v[r][2][col];
+        const double qxn = v[r][1][col + s], qyn = v[r + s][2][col];
+        const double df = fwd ? qxn - qx : qx - qxn, dg = fwd ? qyn - qy : qy - qyn;
+        if (c->exact) return (hh - (dtdx * df + dtdy * dg)) + 0.0;
+        return hh - std::fma(dtdx, df, dtdy * dg);
+    };
+    const double h_min = c->pol.h_min;
+    auto dry = [&](double x) { return !(x >= h_min); };
+    const double own = star_h(0, 0);
+    if (dry(own)) return own;
+    auto face = [&](bool at_edge, int type, int di, int dj, bool uses_nbr) -> double {
+        // wall / inflow faces read no neighbour U*; other edge faces read a ghost
+        // of U*(i, j), which already passed (fixed-elevation ghosts are >= h_min)
+        if (at_edge && (type == SWE_BC_WALL || type == SWE_BC_INFLOW)) return h_min;
+        if (at_edge || !uses_nbr) return h_min;
+        return star_h(di, dj);
+    };
+    const double cand[4] = {face(i == 0, c->bnd.west.type, -1, 0, fwd), face(i == nx - 1, c->bnd.east.type, 1, 0, !fwd),
+                            face(j == 0, c->bnd.south.type, 0, -1, fwd),
+                            face(j == ny - 1, c->bnd.north.type, 0, 1, !fwd)};
+    for (double x : cand)
+        if (dry(x)) return x;
+    return own;
+}
+
 // Translate the control block after a launch into the reference's outcome.
 // Returns SWE_OK (committed), an error, or resolves a diagnosis request.
 int resolve(swe_ctx* c, swe_status* st) {
     SweCtl& h = *c->h_ctl;
     if (h.status == SWE_OK) return SWE_OK;
     if (h.status == SWE_STATUS_DIAG) {
-        // Exact per-cell CFL scan of the candidate (executor.hpp:560-580).
         const int cand = h.sel ^ 1;
+        const bool fwd = (h.step_index % 2) == 0;
+        if (h.diag_flags & 2) {  // K4: an interior window saw a dry U*
+            unsigned long long first = 0;
+            int rc = run_dry_scan(c, h.dt_used, fwd, &first, st);
+            if (rc) return rc;
+            if (first) {
+                const unsigned long long idx = ~first;
+                const int i = static_cast<int>(idx % c->g.nx), j = static_cast<int>(idx / c->g.nx);
+                h.status = SWE_ERR_INSTABILITY;
+                h.err_kind = 4;
+                h.done = 1;
+                write_ctl(c, st);
+                const double hd = dry_star_depth(c, i, j, h.dt_used, fwd);
+                int r = set_status(st, SWE_ERR_INSTABILITY, i, j, h.t_commit,
+                                   "predicted depth %f below dry threshold at cell (%d, %d)", hd, i, j);
+                if (st) st->h = hd;
+                return r;
+            }
+        }
+        // Exact per-cell guard (K5, executor.hpp:543-556) and CFL (K6,
+        // executor.hpp:560-580) scan of the candidate.
         unsigned long long sc[SCAN_N];
         int rc = run_scan(c, cand, sc, st);
         if (rc) return rc;
+        if (sc[SCAN_GUARD]) {
+            const unsigned long long idx = ~sc[SCAN_GUARD];
+            const int i = static_cast<int>(idx % c->g.nx), j = static_cast<int>(idx / c->g.nx);
+            h.status = SWE_ERR_INSTABILITY;
+            h.err_kind = 5;
+            h.done = 1;
+            write_ctl(c, st);
+            double vh, vqx, vqy;
+            cell_values(c, cand, idx, &vh, &vqx, &vqy);
+            int r = set_status(st, SWE_ERR_INSTABILITY, i, j, h.t_commit,
+                               "instability: cell (%d, %d) at t=%f: h=%f qx=%f qy=%f", i, j, h.t_commit, vh, vqx,
+                               vqy);
+            if (st) {
+                st->h = vh;
+                st->qx = vqx;
+                st->qy = vqy;
+            }
+            return r;
+        }
         if (sc[SCAN_BAD]) {
             const unsigned long long idx = ~sc[SCAN_BAD];
             h.status = SWE_ERR_INSTABILITY;
@@ -342,9 +448,13 @@ int resolve(swe_ctx* c, swe_status* st) {
     if (h.status == SWE_ERR_INSTABILITY) {
         if (h.err_kind == 2)
             return set_status(st, SWE_ERR_INSTABILITY, -1, -1, 0.0, "depth below dry threshold");
-        if (h.err_kind == 4)
-            return set_status(st, SWE_ERR_INSTABILITY, h.err_i, h.err_j, h.err_t,
-                              "predicted depth below dry threshold at cell (%d, %d)", h.err_i, h.err_j);
+        if (h.err_kind == 4) {  // require_wet_at's message (executor.hpp:429-436)
+            const double hd = dry_star_depth(c, h.err_i, h.err_j, h.dt_used, (h.step_index % 2) == 0);
+            int r = set_status(st, SWE_ERR_INSTABILITY, h.err_i, h.err_j, h.err_t,
+                               "predicted depth %f below dry threshold at cell (%d, %d)", hd, h.err_i, h.err_j);
+            if (st) st->h = hd;
+            return r;
+        }
         // guard (executor.hpp:889-897): values come from the candidate buffer
         double vh, vqx, vqy;
         cell_values(c, h.sel ^ 1, static_cast<unsigned long long>(h.err_j) * c->g.nx + h.err_i, &vh, &vqx, &vqy);
@@ -638,8 +748,9 @@ int finish_load(swe_ctx* c, double t, swe_status* st) {
     if (!c->d_slope) CUDA_TRY(cudaMalloc(&c->d_slope, static_cast<size_t>(nloc + 2 * R) * 2 * P * sizeof(double)));
     CUDA_TRY(cudaMemsetAsync(c->d_slope, 0, static_cast<size_t>(nloc + 2 * R) * 2 * P * sizeof(double), c->stream));
     CUDA_TRY(cudaMemsetAsync(c->d_flags, 0, 4 * sizeof(unsigned), c->stream));
-    slopes_kernel<<<148 * 4, 256, 0, c->stream>>>(d_zp, c->d_slope, P, R, nx, nloc, c->j0, c->g.ny,
-                                                   2.0 * c->g.dx, 2.0 * c->g.dy, c->d_flags);
+    slopes_kernel<<<std::min(nloc + 2 * R, 148 * 8), 256, 0, c->stream>>>(
+        d_zp, c->d_slope, P, R, nx, nloc, c->j0, c->g.ny, 2.0 * c->g.dx, 2.0 * c->g.dy, c->exact ? 1.0 : -c->ph.g,
+        c->d_flags);
     CUDA_TRY(cudaGetLastError());
     // fixed-elevation clamp diagnostic (grid.hpp:256-263): depends on the bed only
     {
@@ -1002,7 +1113,10 @@ EXPORT int swe_cuda_advance_marked(swe_ctx* c, double t_end, double t_mark, uint
     h.step_index = step_index0;
     h.steps_done = 0;
     h.sel = c->sel;
-    h.done = !(c->t < t_end) || c->t >= t_mark;
+    // t_mark stops the run only after a committed step (the device finalize
+    // and resolve() test it), like run_from's mark check after each step
+    // (run.hpp:159-163): a mark that rounds to <= t still advances one step.
+    h.done = !(c->t < t_end);
     h.status = 0;
     h.finish = 0;
     std::memset(h.red, 0, sizeof h.red);

@@ -18,6 +18,7 @@
 // 0..N-1) over NCCL; `:local` keeps all strips on device 0 and exchanges
 // through the local-group transport instead (single-GPU testing).
 #include <algorithm>
+#include <atomic>
 #include <barrier>
 #include <chrono>
 #include <cmath>
@@ -416,6 +417,7 @@ Report run_scenario(const Scenario& sc, bool write, const Resume* resume = nullp
         }
     }
     std::barrier sync(nr);
+    std::atomic<bool> snap_failed{false};
     std::mutex m;
     std::exception_ptr err;
     const auto wall0 = std::chrono::steady_clock::now();
@@ -460,14 +462,23 @@ Report run_scenario(const Scenario& sc, bool write, const Resume* resume = nullp
                 std::copy(s.z.begin() + a, s.z.begin() + b, shared.z.begin() + a);
                 sync.arrive_and_wait();
                 if (r == 0) {
-                    shared.t = s.t;
-                    const std::string p = snapshot_path(sc, ordinal, final);
-                    if (write) write_snapshot(shared, p, sc.phys.g, dt_next, sidx);
-                    rep.paths.push_back(p);
-                    rep.snapshots = ordinal + 1;
+                    try {
+                        shared.t = s.t;
+                        const std::string p = snapshot_path(sc, ordinal, final);
+                        if (write) write_snapshot(shared, p, sc.phys.g, dt_next, sidx);
+                        rep.paths.push_back(p);
+                        rep.snapshots = ordinal + 1;
+                    } catch (...) {
+                        // every rank leaves the loop together: the others would
+                        // otherwise enter collectives rank 0 never joins
+                        std::lock_guard<std::mutex> lk(m);
+                        if (!err) err = std::current_exception();
+                        snap_failed.store(true);
+                    }
                 }
                 ++ordinal;
                 sync.arrive_and_wait();
+                if (snap_failed.load()) throw DeviceError("run: snapshot write failed on rank 0");
             };
             while (t < sc.t_end) {
                 const RunResult res = st.advance_marked(sc.t_end, mark, sidx, dt_raw);
@@ -475,6 +486,8 @@ Report run_scenario(const Scenario& sc, bool write, const Resume* resume = nullp
                 dt_raw = res.dt_next;
                 t = res.t_final;
                 steps += res.steps;
+                if (res.steps == 0 && t < sc.t_end)
+                    throw DeviceError("run: the device loop committed no step before t_end");
                 if (se > 0.0 && t >= mark && t < sc.t_end) {
                     snap(dt_raw, false);
                     mark = (std::floor(t / se) + 1.0) * se;

@@ -93,7 +93,7 @@ struct BcSet {
 };
 
 // Scan words (max-combined, like the step reduction).
-enum { SCAN_BAD = 0, SCAN_MINR = 1, SCAN_GUARD = 2, SCAN_N = 4 };
+enum { SCAN_BAD = 0, SCAN_MINR = 1, SCAN_GUARD = 2, SCAN_DRY = 3, SCAN_N = 4 };
 
 constexpr int kMaxLocalRanks = 16;  // ranks of a local strip group
 struct RedPtrs {
@@ -106,7 +106,7 @@ __global__ void ghost_fill_rows_kernel(double* b, int P, int R, int nx, int nloc
                                        const double* z_e, const double* z_s, const double* z_n,
                                        double h_min);
 __global__ void slopes_kernel(const double* zp, double* slope, int P, int R, int nx, int nloc,
-                              int j0, int ny, double two_dx, double two_dy, unsigned* flags);
+                              int j0, int ny, double two_dx, double two_dy, double scale, unsigned* flags);
 __global__ void item_flat_kernel(const double* slope, int P, int R, int nx, int nloc, int TW, int chunk,
                                  int ntiles, int nitems, unsigned char* flat);
 __global__ void item_elig_kernel(const unsigned char* flat, int nx, int nloc, int TW, int chunk, int ntiles,
@@ -117,6 +117,10 @@ __global__ void clamp_kernel(const double* zp, int R, int nx, int nloc, int own_
 __global__ void initial_kernel(swe_initial ic, double dx, int nx, int nloc, int P, int R, double* buf, double* zp);
 __global__ void scan_kernel(const double* b, int P, int R, int nx, int nloc, int j0, double g,
                             double dx, double dy, double h_min, unsigned long long* out);
+__global__ void dry_scan_kernel(const double* b, int P, int R, int nx, int ny, int nloc, int j0, double dt,
+                                double dx, double dy, int fwd, int exact, BcSet bs, const double* z_w,
+                                const double* z_e, const double* z_s, const double* z_n, double h_min,
+                                unsigned long long* out);
 __global__ void selftest_div_kernel(const double* a, const double* b, size_t n, int exact, double* out);
 __global__ void max_reduce_kernel(RedPtrs in, int nranks, int n, unsigned long long* out);
 

@@ -134,27 +134,30 @@ __device__ __forceinline__ int seg_list(const StepParams& p, long long w, long l
 __device__ __forceinline__ void finalize_step(const StepParams& p, SweCtl* c, double dt, double tc) {
     volatile unsigned long long* red = c->red;
     const unsigned long long e2 = red[RED_E2], e4 = red[RED_E4], e5 = red[RED_E5];
-    const unsigned long long dg = red[RED_DIAG];
+    const unsigned long long dg = red[RED_DIAG], dry = red[RED_DRY];
     const double msx = __longlong_as_double(static_cast<long long>(red[RED_SX]));
     const double msy = __longlong_as_double(static_cast<long long>(red[RED_SY]));
-    int status = 0, kind = 0, ei = -1, ej = -1;
+    int status = 0, kind = 0, ei = -1, ej = -1, dflags = 0;
     double et = 0.0, edt = 0.0, dt_next = 0.0;
+    // plan order (executor.hpp:846-911): K2 precondition, K4 dry U*, K5 guard, K6
     if (e2) {
         status = SWE_ERR_INSTABILITY; kind = 2;
+    } else if (dry) {
+        // an interior window saw a dry U*: the host finds the row-major first
+        // consumer over the whole grid (dry_scan_kernel), then K5/K6
+        status = SWE_STATUS_DIAG;
+        dflags = 2 | (e5 ? 1 : 0);
     } else if (e4) {
         const unsigned long long idx = ~e4;
         status = SWE_ERR_INSTABILITY; kind = 4;
         ei = static_cast<int>(idx % static_cast<unsigned long long>(p.nx));
         ej = static_cast<int>(idx / static_cast<unsigned long long>(p.nx));
         et = tc;
-    } else if (e5) {
-        const unsigned long long idx = ~e5;
-        status = SWE_ERR_INSTABILITY; kind = 5;
-        ei = static_cast<int>(idx % static_cast<unsigned long long>(p.nx));
-        ej = static_cast<int>(idx / static_cast<unsigned long long>(p.nx));
-        et = tc;
-    } else if (dg || p.always_diag || !(msx < p.tz_x) || !(msy < p.tz_y)) {
+    } else if (e5 || dg || p.always_diag || !(msx < p.tz_x) || !(msy < p.tz_y)) {
+        // guard screen failed (first offender and values from the exact scan)
+        // or dx/sx may round to 0 / overflow: exact per-cell K5 + K6 scan
         status = SWE_STATUS_DIAG;
+        dflags = e5 ? 1 : 0;
     } else {
         const double a = __ddiv_rn(p.dx, msx);
         const double b = __ddiv_rn(p.dy, msy);
@@ -165,6 +168,7 @@ __device__ __forceinline__ void finalize_step(const StepParams& p, SweCtl* c, do
             status = SWE_ERR_STEP_COLLAPSE; kind = 6; edt = dt_raw; et = tc;
         }
     }
+    c->diag_flags = dflags;
     c->max_sx = msx;
     c->max_sy = msy;
     c->dt_used = dt;
@@ -223,6 +227,12 @@ struct Carry {
     CellVec c_dy;              // (dt/dy) * (H_north - H_south) of that row (its y-face term)
     CellVec c_hx;              // its own x face (the other one comes from the neighbour lane)
     CellVec Cp, Cpp;           // corrector output of rows b-S, b-2S (smoothing)
+    // fast mode (classic corrector form, see iter()): G(U*) of the stage-2 row,
+    // carried to the next iteration, and row b's own stage-2 results
+    CellVec Gs;                // G(U*) of row b
+    CellVec c_fs;              // F(U*) of row b (shuffled to the corrector neighbour)
+    CellVec c_sum;             // U + U* of row b
+    double c_ssx, c_ssy;       // S(U*) of row b
 };
 
 struct WarpRing {  // per-warp TMA ring state (warp-uniform)
@@ -232,8 +242,24 @@ struct WarpRing {  // per-warp TMA ring state (warp-uniform)
 
 // BED: 0 flat (no bed reads), 1 both slopes, 2 dz/dx only (dz/dy is +0.0
 // everywhere, e.g. a channel sloping along x: the dz/dy rows are not read)
+#ifndef SWE_FAST_CLASSIC
+#define SWE_FAST_CLASSIC 0
+#endif
+// SWE_ABL (measurement only, wrong results): 1 no output stores, 2 no guard /
+// dry checks, 4 no CFL speeds, 8 no friction on U*, 16 no friction on U
+#ifndef SWE_ABL
+#define SWE_ABL 0
+#endif
+#ifndef SWE_EMIT_MASKED
+#define SWE_EMIT_MASKED 0
+#endif
+#ifndef SWE_CFL_DEFER
+#define SWE_CFL_DEFER 0
+#endif
+
 template <int WPB, bool FWD, bool SMOOTH, int BED, bool MANNING, bool EXACT, bool EARLY>
 struct Marcher {
+    static constexpr bool CLASSIC = SWE_FAST_CLASSIC != 0;  // fast-mode corrector form (see iter())
     static constexpr bool FLAT = BED == 0;
     static constexpr bool XONLY = BED == 2;
     using A = Arith<EXACT>;
@@ -256,7 +282,9 @@ struct Marcher {
     const double* cur;
     double* nxt;
     int P;
-    double dt, dtdx, dtdy, half_dt, h_min, half_g, neg_g, gnn, cx, cy;
+    double dt, dtdx, dtdy, half_dt, cx, cy;
+    // physics constants are read from the kernel parameters (constant-bank
+    // operands, no registers): p.h_min, p.half_g, p.neg_g, p.gnn
     // producer state (warp-uniform): row groups left in the current segment,
     // TMA coordinates of the next request, committed buffer
     int pleft;
@@ -271,16 +299,18 @@ struct Marcher {
     // reductions
     double mx, my;
     int e2;
-    unsigned long long e4, e5;
-    // per-segment row-only error words (this lane's column is fixed within a
-    // segment): ~row of the first offending row, 0 = none; folded into e4/e5
-    // (as ~(row*nx + i)) at the end of the segment
-    unsigned e4r, e5r;
+    unsigned long long e4;  // ~ first dry-U* consumer found in an edge window / row (exact)
+    // screens whose exact first offender the host finds only when they fail:
+    // g_ok = every emitted cell passed the guard screen (h >= h_min and finite
+    // CFL speeds, which is finite h, qx, qy); d_ok = no interior U* was dry
+    bool g_ok, d_ok;
     // quiet-item tracking of the current segment (early exit): with
     // mom = bits(qx) | bits(qy) per output cell, qo |= bits(h) | mom and
     // qn &= bits(h) & ~mom end equal iff every cell is (H, +0, +0), same H
     unsigned long long qo, qn;
     unsigned nitems;  // items of this launch (all, or the active list)
+    CellVec pend;     // SWE_CFL_DEFER: output cell whose CFL speeds are pending
+    bool pvalid;
 
     __device__ __forceinline__ double shf_nb(double x) const {
         return FWD ? __shfl_down_sync(FULL, x, 1) : __shfl_up_sync(FULL, x, 1);
@@ -383,31 +413,47 @@ struct Marcher {
 
     // output cell: guard (K5), CFL (K6), store, ghosts for the next step (K1)
     template <bool EDGE>
-    __device__ __forceinline__ void emit(const CellVec& o, int rr) {
+    // on = false (SWE_EMIT_MASKED, lanes outside the output columns): the
+    // arithmetic runs, the reductions and stores are masked
+    __device__ __forceinline__ void emit(const CellVec& o, int rr, bool on = true) {
         const int jj = p.j0 + rr;
-        double u, v, c;  // executor.hpp:560-580
+        double sx, sy;  // executor.hpp:560-580
+        bool cfl_ok = true;
         if constexpr (EXACT) {
+            double u, v;
             const Rc rc = A::recip(o.h);
-            c = A::sqrt_(p.g * o.h);
+            const double c = A::sqrt_(p.g * o.h);
             A::div2(o.qx, o.qy, rc, u, v);
+            sx = fabs(u) + c;
+            sy = fabs(v) + c;
+        } else if constexpr (SWE_CFL_DEFER) {
+            // the speeds of this row's cell are formed in the next emit (or at
+            // the end of the segment), off this iteration's dependency chain
+            cfl_speeds_fast(pend.h, pend.qx, pend.qy, p.sqrt_g, sx, sy);
+            cfl_ok = pvalid;
+            pend = o;
+            pvalid = true;
+        } else if constexpr ((SWE_ABL & 4) != 0) {
+            sx = o.h;
+            sy = o.qx;
         } else {
-            double rh;
-            cfl_fast(o.h, p.sqrt_g, rh, c);
-            u = o.qx * rh;
-            v = o.qy * rh;
+            cfl_speeds_fast(o.h, o.qx, o.qy, p.sqrt_g, sx, sy);
         }
-        const double sx = fabs(u) + c, sy = fabs(v) + c;
         // guard (executor.hpp:543-558): a non-finite h, qx or qy always makes
         // sx + sy non-finite, so one test screens the cell; the exact test
         // runs only for the rare cell that fails the screen.
         // predicated: no branch splits the iteration's basic block
         {
-            const bool ok = finite_d(o.h) & finite_d(o.qx) & finite_d(o.qy) & (o.h >= h_min);
-            e5r = max(e5r, ok ? 0u : ~static_cast<unsigned>(jj));
+            // h >= h_min also rejects NaN h; the speeds are NaN for a NaN qx, qy
+            // or an infinite h, and an infinite qx makes the CFL maximum
+            // infinite, which sends the step to the exact scan as well
+            const bool ok = (o.h >= p.h_min) & !isnan(sx) & !isnan(sy);
+            if (!(SWE_ABL & 2)) g_ok = g_ok & (ok | !on);
         }
         // CFL maxima; a NaN speed (only in a guarded cell) never replaces them
-        mx = (sx > mx) ? sx : mx;
-        my = (sy > my) ? sy : my;
+        cfl_ok = cfl_ok && on;
+        mx = (cfl_ok && sx > mx) ? sx : mx;
+        my = (cfl_ok && sy > my) ? sy : my;
         if constexpr (EARLY) {
             const unsigned long long hb = dbits(o.h), mom = dbits(o.qx) | dbits(o.qy);
             qo |= hb | mom;
@@ -415,32 +461,35 @@ struct Marcher {
         }
         double* row = orow;  // == nxt + (rr + R) * 3P + (i + R)
         orow += S * 3 * P;
-        row[0] = o.h;
-        row[P] = o.qx;
-        row[2 * P] = o.qy;
+        if (on && !(SWE_ABL & 1)) {
+            row[0] = o.h;
+            row[P] = o.qx;
+            row[2 * P] = o.qy;
+        }
         if constexpr (!EDGE) return;
+        if (!on) return;
         if (!(xedge || jj == 0 || jj == p.ny - 1)) return;
         if (i == 0) {
-            const CellVec g = edge_ghost(SWE_EDGE_W, p.bc[SWE_EDGE_W], o, p.z_w[rr + R], h_min);
+            const CellVec g = edge_ghost(SWE_EDGE_W, p.bc[SWE_EDGE_W], o, p.z_w[rr + R], p.h_min);
             row[-1] = g.h;
             row[P - 1] = g.qx;
             row[2 * P - 1] = g.qy;
         }
         if (i == p.nx - 1) {
-            const CellVec g = edge_ghost(SWE_EDGE_E, p.bc[SWE_EDGE_E], o, p.z_e[rr + R], h_min);
+            const CellVec g = edge_ghost(SWE_EDGE_E, p.bc[SWE_EDGE_E], o, p.z_e[rr + R], p.h_min);
             row[1] = g.h;
             row[P + 1] = g.qx;
             row[2 * P + 1] = g.qy;
         }
         if (jj == 0) {
-            const CellVec g = edge_ghost(SWE_EDGE_S, p.bc[SWE_EDGE_S], o, p.z_s[i], h_min);
+            const CellVec g = edge_ghost(SWE_EDGE_S, p.bc[SWE_EDGE_S], o, p.z_s[i], p.h_min);
             double* gr = row - 3 * P;
             gr[0] = g.h;
             gr[P] = g.qx;
             gr[2 * P] = g.qy;
         }
         if (jj == p.ny - 1) {
-            const CellVec g = edge_ghost(SWE_EDGE_N, p.bc[SWE_EDGE_N], o, p.z_n[i], h_min);
+            const CellVec g = edge_ghost(SWE_EDGE_N, p.bc[SWE_EDGE_N], o, p.z_n[i], p.h_min);
             double* gr = row + 3 * P;
             gr[0] = g.h;
             gr[P] = g.qx;
@@ -465,13 +514,13 @@ struct Marcher {
             if (bc.type == SWE_BC_WALL) {
                 w = {0.0, avg(FU.fxx, FS.fxx), 0.0};
             } else if (bc.type == SWE_BC_INFLOW) {
-                const CellVec a = flux_x_plain(pump_state(SWE_EDGE_W, bc.q_n, U), half_g);
-                const CellVec c = flux_x_plain(pump_state(SWE_EDGE_W, bc.q_n, Us), half_g);
+                const CellVec a = flux_x_plain(pump_state(SWE_EDGE_W, bc.q_n, U), p.half_g);
+                const CellVec c = flux_x_plain(pump_state(SWE_EDGE_W, bc.q_n, Us), p.half_g);
                 w = {avg(a.h, c.h), avg(a.qx, c.qx), avg(a.qy, c.qy)};
             } else if (FWD) {
-                const CellVec g = edge_ghost(SWE_EDGE_W, bc, Us, p.z_w[b + R], h_min);
-                if (!(g.h >= h_min)) e4 = max(e4, ~idx);
-                const CellVec c = flux_x_plain(g, half_g);
+                const CellVec g = edge_ghost(SWE_EDGE_W, bc, Us, p.z_w[b + R], p.h_min);
+                if (!(g.h >= p.h_min)) e4 = max(e4, ~idx);
+                const CellVec c = flux_x_plain(g, p.half_g);
                 w = {avg(U.qx, c.h), avg(FU.fxx, c.qx), avg(FU.fxy, c.qy)};
             } else {
                 set = false;
@@ -488,13 +537,13 @@ struct Marcher {
             if (bc.type == SWE_BC_WALL) {
                 e = {0.0, avg(FU.fxx, FS.fxx), 0.0};
             } else if (bc.type == SWE_BC_INFLOW) {
-                const CellVec a = flux_x_plain(pump_state(SWE_EDGE_E, bc.q_n, U), half_g);
-                const CellVec c = flux_x_plain(pump_state(SWE_EDGE_E, bc.q_n, Us), half_g);
+                const CellVec a = flux_x_plain(pump_state(SWE_EDGE_E, bc.q_n, U), p.half_g);
+                const CellVec c = flux_x_plain(pump_state(SWE_EDGE_E, bc.q_n, Us), p.half_g);
                 e = {avg(a.h, c.h), avg(a.qx, c.qx), avg(a.qy, c.qy)};
             } else if (!FWD) {
-                const CellVec g = edge_ghost(SWE_EDGE_E, bc, Us, p.z_e[b + R], h_min);
-                if (!(g.h >= h_min)) e4 = max(e4, ~idx);
-                const CellVec c = flux_x_plain(g, half_g);
+                const CellVec g = edge_ghost(SWE_EDGE_E, bc, Us, p.z_e[b + R], p.h_min);
+                if (!(g.h >= p.h_min)) e4 = max(e4, ~idx);
+                const CellVec c = flux_x_plain(g, p.half_g);
                 e = {avg(U.qx, c.h), avg(FU.fxx, c.qx), avg(FU.fxy, c.qy)};
             } else {
                 set = false;
@@ -511,13 +560,13 @@ struct Marcher {
             if (bc.type == SWE_BC_WALL) {
                 f = {0.0, 0.0, avg(FU.gyy, FS.gyy)};
             } else if (bc.type == SWE_BC_INFLOW) {
-                const CellVec a = flux_y_plain(pump_state(SWE_EDGE_S, bc.q_n, U), half_g);
-                const CellVec c = flux_y_plain(pump_state(SWE_EDGE_S, bc.q_n, Us), half_g);
+                const CellVec a = flux_y_plain(pump_state(SWE_EDGE_S, bc.q_n, U), p.half_g);
+                const CellVec c = flux_y_plain(pump_state(SWE_EDGE_S, bc.q_n, Us), p.half_g);
                 f = {avg(a.h, c.h), avg(a.qx, c.qx), avg(a.qy, c.qy)};
             } else if (FWD) {
-                const CellVec g = edge_ghost(SWE_EDGE_S, bc, Us, p.z_s[i], h_min);
-                if (!(g.h >= h_min)) e4 = max(e4, ~idx);
-                const CellVec c = flux_y_plain(g, half_g);
+                const CellVec g = edge_ghost(SWE_EDGE_S, bc, Us, p.z_s[i], p.h_min);
+                if (!(g.h >= p.h_min)) e4 = max(e4, ~idx);
+                const CellVec c = flux_y_plain(g, p.half_g);
                 f = {avg(U.qy, c.h), avg(FU.fxy, c.qx), avg(FU.gyy, c.qy)};
             } else {
                 set = false;
@@ -534,13 +583,13 @@ struct Marcher {
             if (bc.type == SWE_BC_WALL) {
                 f = {0.0, 0.0, avg(FU.gyy, FS.gyy)};
             } else if (bc.type == SWE_BC_INFLOW) {
-                const CellVec a = flux_y_plain(pump_state(SWE_EDGE_N, bc.q_n, U), half_g);
-                const CellVec c = flux_y_plain(pump_state(SWE_EDGE_N, bc.q_n, Us), half_g);
+                const CellVec a = flux_y_plain(pump_state(SWE_EDGE_N, bc.q_n, U), p.half_g);
+                const CellVec c = flux_y_plain(pump_state(SWE_EDGE_N, bc.q_n, Us), p.half_g);
                 f = {avg(a.h, c.h), avg(a.qx, c.qx), avg(a.qy, c.qy)};
             } else if (!FWD) {
-                const CellVec g = edge_ghost(SWE_EDGE_N, bc, Us, p.z_n[i], h_min);
-                if (!(g.h >= h_min)) e4 = max(e4, ~idx);
-                const CellVec c = flux_y_plain(g, half_g);
+                const CellVec g = edge_ghost(SWE_EDGE_N, bc, Us, p.z_n[i], p.h_min);
+                if (!(g.h >= p.h_min)) e4 = max(e4, ~idx);
+                const CellVec c = flux_y_plain(g, p.half_g);
                 f = {avg(U.qy, c.h), avg(FU.fxy, c.qx), avg(FU.gyy, c.qy)};
             } else {
                 set = false;
@@ -562,8 +611,8 @@ struct Marcher {
             // ======== stage 1: committed row b+S
             consume<GI>(out.U, out.zx, out.zy);
             const Rc rcN = A::recip(out.U.h);
-            out.FU = A::flux(out.U, rcN, half_g);
-            source_of<EXACT, MANNING, FLAT, FLAT || XONLY>(out.U, out.FU, rcN, out.zx, out.zy, neg_g, gnn, out.srx, out.sry);
+            out.FU = A::template flux<MANNING>(out.U, rcN, p.half_g);
+            source_of<EXACT, MANNING && !(SWE_ABL & 16), FLAT, FLAT || XONLY>(out.U, out.FU, rcN, out.zx, out.zy, p.neg_g, p.gnn, out.srx, out.sry);
 
             // ======== stage 2: predictor at (i, b)   scheme.hpp:100-113
             const CellVec& U = in.U;
@@ -595,9 +644,10 @@ struct Marcher {
             const int jb = p.j0 + b;
             // dry U* -> row-major first consumer (executor.hpp:429-436, 459-513)
             if constexpr (!EDGE) {  // interior rows: jb >= 1, consumer is the row-major next cell
-                const bool dry = !(Us.h >= h_min) & star_ok;
-                e4r = max(e4r, dry ? ~static_cast<unsigned>(FWD ? jb : jb - 1) : 0u);
-            } else if (!(Us.h >= h_min) && star_ok && (!EDGE || (in_x && jb >= 0 && jb < p.ny))) {
+                // every lane's U* is a real interior U* here, consumed by some
+                // corrector cell: a flag, the host finds the first consumer
+                if (!(SWE_ABL & 2)) d_ok = d_ok & (Us.h >= p.h_min);
+            } else if (!(Us.h >= p.h_min) && star_ok && (!EDGE || (in_x && jb >= 0 && jb < p.ny))) {
                 unsigned long long cons;
                 if (FWD) cons = static_cast<unsigned long long>(jb) * p.nx + i;
                 else if (jb >= 1) cons = static_cast<unsigned long long>(jb - 1) * p.nx + i;
@@ -606,66 +656,151 @@ struct Marcher {
                 e4 = max(e4, ~cons);
             }
             // K2 precondition on the committed state (scheme.hpp:35-39)
-            e2 |= static_cast<int>(!(U.h >= h_min) & (k >= 0) & (k < L) & out_x);
+            if constexpr (!EDGE) {
+                // interior windows: every lane and march row is a domain cell
+                // the reference's predictor reads
+                if (!(SWE_ABL & 2)) e2 |= static_cast<int>(!(U.h >= p.h_min));
+            } else {
+                e2 |= static_cast<int>(!(U.h >= p.h_min) & (k >= 0) & (k < L) & out_x);
+            }
 
             const Rc rcS = A::recip(Us.h);
-            const Flux FS = A::flux(Us, rcS, half_g);
+            const Flux FS = A::template flux<MANNING>(Us, rcS, p.half_g);
             double ssx, ssy;
-            source_of<EXACT, MANNING, FLAT, FLAT || XONLY>(Us, FS, rcS, in.zx, in.zy, neg_g, gnn, ssx, ssy);
+            source_of<EXACT, MANNING && !(SWE_ABL & 8), FLAT, FLAT || XONLY>(Us, FS, rcS, in.zx, in.zy, p.neg_g, p.gnn, ssx, ssy);
 
-            // own x face (FWD: east, BWD: west) and y face (b, b+S)   scheme.hpp:153-161
-            CellVec Hx = {avg(fn_h, Us.qx), avg(fn_qx, FS.fxx), avg(fn_qy, FS.fxy)};
-            out.Hyp = {avg(Un.qy, Us.qy), avg(FN.fxy, FS.fxy), avg(FN.gyy, FS.gyy)};
-            CellVec hy_a = in.Hyp, hy_b = out.Hyp;  // faces (b-S, b) and (b, b+S)
-            if (EDGE && (xedge || jb == 0 || jb == p.ny - 1)) {  // warp-uniform
-                CellVec xo = {0.0, 0.0, 0.0};
-                int give = 0;
-                boundary_faces(b, jb, U, FU, Us, FS, Hx, hy_a, hy_b, xo, give);
-                if (xedge) {  // hand the boundary face to the out-of-domain lane that owns it
-                    const double gh = shf_nb(xo.h), gqx = shf_nb(xo.qx), gqy = shf_nb(xo.qy);
-                    const int gv = FWD ? __shfl_down_sync(FULL, give, 1) : __shfl_up_sync(FULL, give, 1);
-                    if (gv && i == (FWD ? -1 : p.nx)) Hx = {gh, gqx, gqy};
+            if constexpr (EXACT || !CLASSIC) {
+                // own x face (FWD: east, BWD: west) and y face (b, b+S)   scheme.hpp:153-161
+                CellVec Hx = {avg(fn_h, Us.qx), avg(fn_qx, FS.fxx), avg(fn_qy, FS.fxy)};
+                out.Hyp = {avg(Un.qy, Us.qy), avg(FN.fxy, FS.fxy), avg(FN.gyy, FS.gyy)};
+                CellVec hy_a = in.Hyp, hy_b = out.Hyp;  // faces (b-S, b) and (b, b+S)
+                if (EDGE && (xedge || jb == 0 || jb == p.ny - 1)) {  // warp-uniform
+                    CellVec xo = {0.0, 0.0, 0.0};
+                    int give = 0;
+                    boundary_faces(b, jb, U, FU, Us, FS, Hx, hy_a, hy_b, xo, give);
+                    if (xedge) {  // hand the boundary face to the out-of-domain lane that owns it
+                        const double gh = shf_nb(xo.h), gqx = shf_nb(xo.qx), gqy = shf_nb(xo.qy);
+                        const int gv = FWD ? __shfl_down_sync(FULL, give, 1) : __shfl_up_sync(FULL, give, 1);
+                        if (gv && i == (FWD ? -1 : p.nx)) Hx = {gh, gqx, gqy};
+                    }
+                }
+                // the corrector's y-face term and source sum are formed here, so row c
+                // carries 8 doubles less into stage 3 (same operations, same order)
+                {
+                    const CellVec& hs = FWD ? hy_a : hy_b;
+                    const CellVec& hn = FWD ? hy_b : hy_a;
+                    out.c_dy = {cy * (hn.h - hs.h), cy * (hn.qx - hs.qx), cy * (hn.qy - hs.qy)};
+                }
+                out.c_hx = Hx;
+                out.Uc = U;
+                out.c_sx = in.srx + ssx;
+                out.c_sy = in.sry + ssy;
+            } else {
+                // FAST: the classic MacCormack corrector (see stage 3) needs F(U*)
+                // and G(U*) of row b, U + U* and S(U*); the face form runs only
+                // for cells with a boundary face (EDGE windows / rows)
+                out.Gs = {Us.qy, FS.fxy, FS.gyy};
+                out.c_fs = {Us.qx, FS.fxx, FS.fxy};
+                out.c_sum = {U.h + Us.h, U.qx + Us.qx, U.qy + Us.qy};
+                out.c_ssx = ssx;
+                out.c_ssy = ssy;
+                if (EDGE && (xedge || jb == 0 || jb == p.ny - 1)) {  // warp-uniform
+                    CellVec Hx = {avg(fn_h, Us.qx), avg(fn_qx, FS.fxx), avg(fn_qy, FS.fxy)};
+                    // face (b-S, b) from G(U_b) and G(U*_{b-S}) (bit-identical to
+                    // the exact path's carried face), face (b, b+S)
+                    CellVec hy_a = {avg(U.qy, in.Gs.h), avg(FU.fxy, in.Gs.qx), avg(FU.gyy, in.Gs.qy)};
+                    CellVec hy_b = {avg(Un.qy, Us.qy), avg(FN.fxy, FS.fxy), avg(FN.gyy, FS.gyy)};
+                    CellVec xo = {0.0, 0.0, 0.0};
+                    int give = 0;
+                    boundary_faces(b, jb, U, FU, Us, FS, Hx, hy_a, hy_b, xo, give);
+                    if (xedge) {
+                        const double gh = shf_nb(xo.h), gqx = shf_nb(xo.qx), gqy = shf_nb(xo.qy);
+                        const int gv = FWD ? __shfl_down_sync(FULL, give, 1) : __shfl_up_sync(FULL, give, 1);
+                        if (gv && i == (FWD ? -1 : p.nx)) Hx = {gh, gqx, gqy};
+                    }
+                    const CellVec& hs = FWD ? hy_a : hy_b;
+                    const CellVec& hn = FWD ? hy_b : hy_a;
+                    out.c_dy = {cy * (hn.h - hs.h), cy * (hn.qx - hs.qx), cy * (hn.qy - hs.qy)};
+                    out.c_hx = Hx;
+                    out.Uc = U;
+                    out.c_sx = in.srx + ssx;
+                    out.c_sy = in.sry + ssy;
                 }
             }
-            // the corrector's y-face term and source sum are formed here, so row c
-            // carries 8 doubles less into stage 3 (same operations, same order)
-            {
-                const CellVec& hs = FWD ? hy_a : hy_b;
-                const CellVec& hn = FWD ? hy_b : hy_a;
-                out.c_dy = {cy * (hn.h - hs.h), cy * (hn.qx - hs.qx), cy * (hn.qy - hs.qy)};
-            }
-            out.c_hx = Hx;
-            out.Uc = U;
-            out.c_sx = in.srx + ssx;
-            out.c_sy = in.sry + ssy;
         }
 
         if constexpr (DO3) {
             // ======== stage 3: corrector of row b   scheme.hpp:185-191
             const Carry& cc = out;  // row b's own stage-2 results (two-stage march)
-            const CellVec ot = {shf_back(cc.c_hx.h), shf_back(cc.c_hx.qx), shf_back(cc.c_hx.qy)};
-            const CellVec hw = FWD ? ot : cc.c_hx, he = FWD ? cc.c_hx : ot;
             CellVec C;
-            // exact: cx = dt/dx, cy = dt/dy (scheme.hpp:185-191 evaluation order);
-            // fast: faces are plain sums, cx = dt/(2dx), cy = dt/(2dy)
-            if constexpr (EXACT) {
-                const double fs_h = cx * (he.h - hw.h) + cc.c_dy.h;
-                const double fs_qx = cx * (he.qx - hw.qx) + cc.c_dy.qx;
-                const double fs_qy = cx * (he.qy - hw.qy) + cc.c_dy.qy;
-                C.h = (cc.Uc.h - fs_h) + 0.0;
-                C.qx = (cc.Uc.qx - fs_qx) + half_dt * cc.c_sx;
-                C.qy = (cc.Uc.qy - fs_qy) + half_dt * cc.c_sy;
+            if constexpr (EXACT || !CLASSIC) {
+                const CellVec ot = {shf_back(cc.c_hx.h), shf_back(cc.c_hx.qx), shf_back(cc.c_hx.qy)};
+                const CellVec hw = FWD ? ot : cc.c_hx, he = FWD ? cc.c_hx : ot;
+                if constexpr (EXACT) {
+                    // cx = dt/dx, cy = dt/dy (scheme.hpp:185-191 evaluation order)
+                    const double fs_h = cx * (he.h - hw.h) + cc.c_dy.h;
+                    const double fs_qx = cx * (he.qx - hw.qx) + cc.c_dy.qx;
+                    const double fs_qy = cx * (he.qy - hw.qy) + cc.c_dy.qy;
+                    C.h = (cc.Uc.h - fs_h) + 0.0;
+                    C.qx = (cc.Uc.qx - fs_qx) + half_dt * cc.c_sx;
+                    C.qy = (cc.Uc.qy - fs_qy) + half_dt * cc.c_sy;
+                } else {  // faces are plain sums, cx = dt/(2dx), cy = dt/(2dy)
+                    const double fs_h = __fma_rn(cx, he.h - hw.h, cc.c_dy.h);
+                    const double fs_qx = __fma_rn(cx, he.qx - hw.qx, cc.c_dy.qx);
+                    const double fs_qy = __fma_rn(cx, he.qy - hw.qy, cc.c_dy.qy);
+                    C.h = cc.Uc.h - fs_h;
+                    C.qx = __fma_rn(half_dt, cc.c_sx, cc.Uc.qx - fs_qx);
+                    C.qy = __fma_rn(half_dt, cc.c_sy, cc.Uc.qy - fs_qy);
+                }
             } else {
-                const double fs_h = __fma_rn(cx, he.h - hw.h, cc.c_dy.h);
-                const double fs_qx = __fma_rn(cx, he.qx - hw.qx, cc.c_dy.qx);
-                const double fs_qy = __fma_rn(cx, he.qy - hw.qy, cc.c_dy.qy);
-                C.h = cc.Uc.h - fs_h;
-                C.qx = __fma_rn(half_dt, cc.c_sx, cc.Uc.qx - fs_qx);
-                C.qy = __fma_rn(half_dt, cc.c_sy, cc.Uc.qy - fs_qy);
+                // FAST: with the interface fluxes H = (F(U) + F(U*))/2 expanded,
+                // the face differences are the predictor's own differences plus
+                // those of F(U*), G(U*), and the update collapses to the classic
+                // MacCormack corrector
+                //   U^{n+1} = (U + U*)/2 - cx dF* - cy dG* + (dt/2) S(U*)
+                // (cx = dt/(2dx), cy = dt/(2dy); dF* the difference of F(U*) in
+                // the corrector's direction).  Cells with a boundary face keep the
+                // face form (boundary_faces), so every cell's arithmetic depends
+                // only on its position, not on the work decomposition.
+                const CellVec fb = {shf_back(cc.c_fs.h), shf_back(cc.c_fs.qx), shf_back(cc.c_fs.qy)};
+                const CellVec& gp = in.Gs;  // G(U*) of row b - S
+                CellVec dF, dG;
+                if constexpr (FWD) {
+                    dF = {cc.c_fs.h - fb.h, cc.c_fs.qx - fb.qx, cc.c_fs.qy - fb.qy};
+                    dG = {cc.Gs.h - gp.h, cc.Gs.qx - gp.qx, cc.Gs.qy - gp.qy};
+                } else {
+                    dF = {fb.h - cc.c_fs.h, fb.qx - cc.c_fs.qx, fb.qy - cc.c_fs.qy};
+                    dG = {gp.h - cc.Gs.h, gp.qx - cc.Gs.qx, gp.qy - cc.Gs.qy};
+                }
+                const double t_h = __fma_rn(cx, dF.h, cy * dG.h);
+                const double t_qx = __fma_rn(cx, dF.qx, cy * dG.qx);
+                const double t_qy = __fma_rn(cx, dF.qy, cy * dG.qy);
+                C.h = __fma_rn(0.5, cc.c_sum.h, -t_h);
+                C.qx = __fma_rn(0.5, cc.c_sum.qx, __fma_rn(half_dt, cc.c_ssx, -t_qx));
+                C.qy = __fma_rn(0.5, cc.c_sum.qy, __fma_rn(half_dt, cc.c_ssy, -t_qy));
+                if constexpr (EDGE) {
+                    const int jb = p.j0 + b;
+                    if (xedge || jb == 0 || jb == p.ny - 1) {  // warp-uniform
+                        const CellVec ot = {shf_back(cc.c_hx.h), shf_back(cc.c_hx.qx), shf_back(cc.c_hx.qy)};
+                        const CellVec hw = FWD ? ot : cc.c_hx, he = FWD ? cc.c_hx : ot;
+                        if (i == 0 || i == p.nx - 1 || jb == 0 || jb == p.ny - 1) {
+                            const double fs_h = __fma_rn(cx, he.h - hw.h, cc.c_dy.h);
+                            const double fs_qx = __fma_rn(cx, he.qx - hw.qx, cc.c_dy.qx);
+                            const double fs_qy = __fma_rn(cx, he.qy - hw.qy, cc.c_dy.qy);
+                            C.h = cc.Uc.h - fs_h;
+                            C.qx = __fma_rn(half_dt, cc.c_sx, cc.Uc.qx - fs_qx);
+                            C.qy = __fma_rn(half_dt, cc.c_sy, cc.Uc.qy - fs_qy);
+                        }
+                    }
+                }
             }
             const int c_row = b;
             if constexpr (!SMOOTH) {
-                if (EMIT && out_x) emit<EDGE>(C, c_row);
+                if constexpr (SWE_EMIT_MASKED) {
+                    if (EMIT) emit<EDGE>(C, c_row, out_x);
+                } else {
+                    if (EMIT && out_x) emit<EDGE>(C, c_row);
+                }
             } else {
                 // smoothing of row q = c - S   (executor.hpp:533-540, scheme.hpp:197-204)
                 const CellVec& Cp = in.Cp;
@@ -680,10 +815,10 @@ struct Marcher {
                         CellVec cn = FWD ? C : in.Cpp;
                         CellVec cs = FWD ? in.Cpp : C;
                         if (EDGE && (xedge || jq == 0 || jq == p.ny - 1)) {
-                            if (i == 0) cw = edge_ghost(SWE_EDGE_W, p.bc[SWE_EDGE_W], Cp, p.z_w[q + R], h_min);
-                            if (i == p.nx - 1) ce = edge_ghost(SWE_EDGE_E, p.bc[SWE_EDGE_E], Cp, p.z_e[q + R], h_min);
-                            if (jq == 0) cs = edge_ghost(SWE_EDGE_S, p.bc[SWE_EDGE_S], Cp, p.z_s[i], h_min);
-                            if (jq == p.ny - 1) cn = edge_ghost(SWE_EDGE_N, p.bc[SWE_EDGE_N], Cp, p.z_n[i], h_min);
+                            if (i == 0) cw = edge_ghost(SWE_EDGE_W, p.bc[SWE_EDGE_W], Cp, p.z_w[q + R], p.h_min);
+                            if (i == p.nx - 1) ce = edge_ghost(SWE_EDGE_E, p.bc[SWE_EDGE_E], Cp, p.z_e[q + R], p.h_min);
+                            if (jq == 0) cs = edge_ghost(SWE_EDGE_S, p.bc[SWE_EDGE_S], Cp, p.z_s[i], p.h_min);
+                            if (jq == p.ny - 1) cn = edge_ghost(SWE_EDGE_N, p.bc[SWE_EDGE_N], Cp, p.z_n[i], p.h_min);
                         }
                         const double nu = p.nu;
                         CellVec o;
@@ -719,19 +854,23 @@ struct Marcher {
         orow = nxt + static_cast<size_t>(r_start + R) * 3 * P + (i + R);  // first output row
         qo = 0ull;
         qn = ~0ull;
-        e4r = e5r = 0u;
         const int jlo = p.j0 + sg.ra - R - 1, jhi = p.j0 + sg.rb + R;  // rows the march touches, padded
         if (xedge || jlo <= 0 || jhi >= p.ny - 1) march<true>();
         else march<false>();
-        if (e4r) e4 = max(e4, ~(static_cast<unsigned long long>(~e4r) * p.nx + i));
-        if (e5r) e5 = max(e5, ~(static_cast<unsigned long long>(~e5r) * p.nx + i));
+        if constexpr (!EXACT && SWE_CFL_DEFER) {  // the segment's last pending cell
+            double sx, sy;
+            cfl_speeds_fast(pend.h, pend.qx, pend.qy, p.sqrt_g, sx, sy);
+            mx = (pvalid && sx > mx) ? sx : mx;
+            my = (pvalid && sy > my) ? sy : my;
+            pvalid = false;
+        }
         if constexpr (EARLY) {
             // quiet flag of this item in the candidate buffer: the depth bits
-            // H when every output cell is (H, +0, +0) with H >= h_min, else 0
+            // H when every output cell is (H, +0, +0) with H >= p.h_min, else 0
             const unsigned long long ref = __shfl_sync(FULL, qo, R);  // lane R is always an output lane
             const bool ok = !out_x || (qo == qn && qo == ref);
             const double H = __longlong_as_double(static_cast<long long>(ref));
-            const bool quiet = __all_sync(FULL, ok) && H >= h_min && finite_d(H);
+            const bool quiet = __all_sync(FULL, ok) && H >= p.h_min && finite_d(H);
             if (lane == 0)
                 p.qflag[sel ^ 1][(sg.ra / p.chunk) * p.ntiles + sg.tile] = quiet ? ref : 0ull;
         }
@@ -744,10 +883,11 @@ struct Marcher {
         consume<0>(A.U, A.zx, A.zy);  // march row 0
         {
             const Rc rc = A::recip(A.U.h);
-            A.FU = A::flux(A.U, rc, half_g);
-            source_of<EXACT, MANNING, FLAT, FLAT || XONLY>(A.U, A.FU, rc, A.zx, A.zy, neg_g, gnn, A.srx, A.sry);
+            A.FU = A::template flux<MANNING>(A.U, rc, p.half_g);
+            source_of<EXACT, MANNING, FLAT, FLAT || XONLY>(A.U, A.FU, rc, A.zx, A.zy, p.neg_g, p.gnn, A.srx, A.sry);
         }
         A.Hyp = {0.0, 0.0, 0.0};
+        A.Gs = {0.0, 0.0, 0.0};
         A.Cp = {0.0, 0.0, 0.0};
         A.Cpp = {0.0, 0.0, 0.0};
         // corrector of row b in the same iteration as its predictor.  Row GI of
@@ -860,10 +1000,6 @@ __global__ void __launch_bounds__(WPB * 32, (step_min_blocks<EXACT, BED == 0, MA
     m.half_dt = 0.5 * m.dt;
     m.cx = EXACT ? m.dtdx : 0.5 * m.dtdx;
     m.cy = EXACT ? m.dtdy : 0.5 * m.dtdy;
-    m.h_min = p.h_min;
-    m.half_g = p.half_g;
-    m.neg_g = p.neg_g;
-    m.gnn = p.gnn;
     m.pleft = 0;
     m.pdone = false;
     m.pn = 0;
@@ -872,10 +1008,14 @@ __global__ void __launch_bounds__(WPB * 32, (step_min_blocks<EXACT, BED == 0, MA
     m.mx = 0.0;
     m.my = 0.0;
     m.e2 = 0;
-    m.e4 = m.e5 = 0ull;
+    m.e4 = 0ull;
+    m.g_ok = true;
+    m.d_ok = true;
     m.nitems = EARLY ? s_nact : static_cast<unsigned>(p.ntiles) * static_cast<unsigned>(p.nchunks);  // this launch's items
     m.qo = 0ull;
     m.qn = ~0ull;
+    m.pend = {1.0, 0.0, 0.0};
+    m.pvalid = false;
     m.produce();
     while (m.qhead < m.qtail) {  // the producer keeps the queue ahead of the consumer
         const Seg sg = m.segq[m.qhead % M::QN];
@@ -895,7 +1035,8 @@ __global__ void __launch_bounds__(WPB * 32, (step_min_blocks<EXACT, BED == 0, MA
     }
     if (m.e2) atomicMax(&ctl->red[RED_E2], 1ull);
     if (m.e4) atomicMax(&ctl->red[RED_E4], m.e4);
-    if (m.e5) atomicMax(&ctl->red[RED_E5], m.e5);
+    if (!m.g_ok) atomicMax(&ctl->red[RED_E5], 1ull);
+    if (!m.d_ok) atomicMax(&ctl->red[RED_DRY], 1ull);
     __syncthreads();
     if (tid == 0) {
         double a = s_red[0][0], b = s_red[1][0];
@@ -967,8 +1108,7 @@ __global__ void __launch_bounds__(256) swe_schedule_kernel(const __grid_constant
                 if constexpr (EXACT) {
                     s = Arith<EXACT>::sqrt_(p.g * H);
                 } else {
-                    double rh;
-                    cfl_fast(H, p.sqrt_g, rh, s);
+                    s = cfl_quiet_fast(H, p.sqrt_g);
                 }
                 smax = (s > smax) ? s : smax;
                 const int ra = rc * p.chunk, rb = min(ra + p.chunk, p.nloc);

@@ -22,10 +22,13 @@ struct SweBC {
 enum {
     RED_SX = 0,   // bits of max sx = |qx/h| + sqrt(g h)   (non-negative doubles order like u64)
     RED_SY = 1,   // bits of max sy
-    RED_E4 = 2,   // ~ first corrector cell consuming a dry U*   (executor.hpp:429-436)
-    RED_E5 = 3,   // ~ first guard offender                       (executor.hpp:543-556)
+    RED_E4 = 2,   // ~ first corrector cell consuming a dry U*, found in an edge window or row
+                  //   (executor.hpp:429-436)
+    RED_E5 = 3,   // 1: the guard screen failed somewhere (executor.hpp:543-556); the first
+                  //   offender is found by the exact scan (scan_kernel)
     RED_E2 = 4,   // committed depth below h_min seen by the predictor (scheme.hpp:35-39)
     RED_DIAG = 5, // K6 needs the exact per-cell scan (dx/sx underflow/overflow possible)
+    RED_DRY = 6,  // 1: an interior U* was dry; the first consumer is found by dry_scan_kernel
     RED_N = 8
 };
 
@@ -55,6 +58,8 @@ struct __align__(16) SweCtl {
     unsigned int work[2];         // dynamic work-item counters (slot per concurrent step launch)
     unsigned int nactive;         // early exit: length of the step's active item list
     unsigned long long red[RED_N];
+    int diag_flags;               // status 7: 1 = guard screen failed, 2 = interior dry U*
+    int pad_;
 };
 
 #define SWE_STATUS_DIAG 7
