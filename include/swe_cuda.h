@@ -253,6 +253,13 @@ int swe_cuda_activity(swe_ctx* ctx, swe_activity* out);
 void swe_cuda_rows(const swe_ctx* ctx, int32_t* row_begin, int32_t* row_end);
 /* Committed-halo radius in rows (1 without smoothing, 2 with). */
 int32_t swe_cuda_halo_rows(const swe_ctx* ctx);
+/* Order-independent 64-bit digest of this rank's committed h, qx, qy bit
+ * patterns: the sum (mod 2^64) over owned cells of a splitmix64 mix of the
+ * three bit patterns and the global cell index j*nx + i.  The digest of the
+ * whole grid is the sum of the ranks' digests, so a strip run and a
+ * one-domain run can be compared bit for bit without copying the state to the
+ * host (no reference counterpart; a checksum for size-independent parity). */
+int swe_cuda_state_digest(swe_ctx* ctx, uint64_t* digest, swe_status* st);
 
 /* ---- multi-GPU plumbing ---------------------------------------------- */
 /* ncclGetUniqueId into out[SWE_NCCL_ID_BYTES] (rank 0 broadcasts it). */

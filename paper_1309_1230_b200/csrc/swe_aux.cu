@@ -303,6 +303,30 @@ __global__ void dry_scan_kernel(const double* b, int P, int R, int nx, int ny, i
     if ((threadIdx.x & 31) == 0 && first) atomicMax(&out[SCAN_DRY], first);
 }
 
+__device__ __forceinline__ unsigned long long splitmix64(unsigned long long x) {
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+
+// swe_cuda_state_digest: sum over owned cells of mix(h, qx, qy, global index).
+__global__ void digest_kernel(const double* b, int P, int R, int nx, int nloc, int j0, unsigned long long* out) {
+    unsigned long long acc = 0;
+    for (int lr = blockIdx.x; lr < nloc; lr += gridDim.x) {
+        const double* hr = b + pidx(P, R, lr, 0, 0);
+        const unsigned long long row0 = static_cast<unsigned long long>(j0 + lr) * nx;
+        for (int i = threadIdx.x; i < nx; i += blockDim.x) {
+            unsigned long long x = splitmix64(row0 + i);
+            x = splitmix64(x ^ swe_dev::dbits(hr[i]));
+            x = splitmix64(x ^ swe_dev::dbits(hr[P + i]));
+            acc += splitmix64(x ^ swe_dev::dbits(hr[2 * P + i]));
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
+}
+
 // Shared-reciprocal division of the step kernels (swe_device.cuh), exposed for
 // the parity self-test.  Compiled with -fmad=false like the exact kernels.
 __global__ void selftest_div_kernel(const double* a, const double* b, size_t n, int exact, double* out) {

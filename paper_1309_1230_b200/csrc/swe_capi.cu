@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -194,14 +195,18 @@ double* row_ptr(swe_ctx* c, int which, int lr) {
 
 // Exchange R committed rows with the strip neighbours:
 // own top rows -> rank+1's lower halo, own bottom rows -> rank-1's upper halo.
+// (c->halo_x rows: R, or fewer under the SWE_DEBUG_HALO_ROWS test hook, which
+// must then break the strips' equality with one domain: the halo-mutation
+// check of test_executor.cpp:246-303.)
 int halo_exchange(swe_ctx* c, int which, cudaStream_t s, swe_status* st) {
     if (c->ex.nranks <= 1) return SWE_OK;
-    const size_t bytes = static_cast<size_t>(c->R) * 3 * c->pitch * sizeof(double);
+    const int rows = c->halo_x;
+    const size_t bytes = static_cast<size_t>(rows) * 3 * c->pitch * sizeof(double);
     const int rk = c->ex.rank, nr = c->ex.nranks;
     const bool up = rk + 1 < nr, down = rk > 0;
-    return c->tr->sendrecv(c, s, up ? row_ptr(c, which, c->nloc - c->R) : nullptr,
+    return c->tr->sendrecv(c, s, up ? row_ptr(c, which, c->nloc - rows) : nullptr,
                            up ? row_ptr(c, which, c->nloc) : nullptr, down ? row_ptr(c, which, 0) : nullptr,
-                           down ? row_ptr(c, which, -c->R) : nullptr, bytes, st);
+                           down ? row_ptr(c, which, -rows) : nullptr, bytes, st);
 }
 
 // Enqueue one step on the stream (no host sync).  `fwd` = sweep parity,
@@ -478,36 +483,50 @@ int resolve(swe_ctx* c, swe_status* st) {
 }
 
 int destroy_graphs(swe_ctx* c) {
-    for (auto& gph : c->graph)
-        if (gph) {
-            cudaGraphExecDestroy(gph);
-            gph = nullptr;
-        }
-    c->graph_len = 0;
+    for (auto& kv : c->graphs)
+        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    c->graphs.clear();
     return 0;
 }
 
-int build_graphs(swe_ctx* c, int len, swe_status* st) {
-    destroy_graphs(c);
-    const unsigned long long before = c->launches;
-    for (int start = 0; start < 2; ++start) {  // start 0: first launch forward
+// The graph of `len` steps whose first step has sweep parity `parity` and
+// finds the committed selector at `sel` (only strips depend on sel).
+int get_graph(swe_ctx* c, int len, int parity, int sel, swe_ctx::Graph** out, swe_status* st) {
+    if (c->ex.nranks == 1) sel = 0;  // one rank: the kernels read the selector on the device
+    const int key = (len << 2) | (parity << 1) | sel;
+    auto it = c->graphs.find(key);
+    if (it == c->graphs.end()) {
+        const unsigned long long before = c->launches;
         cudaGraph_t gph;
         CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
         int rc = SWE_OK;
-        for (int k = 0; k < len && rc == SWE_OK; ++k) {
-            const bool fwd = ((start + k) % 2) == 0;
-            rc = enqueue_step(c, fwd, (k + 1) & 1, st);  // candidate relative to sel: see advance()
-        }
+        for (int k = 0; k < len && rc == SWE_OK; ++k)
+            rc = enqueue_step(c, ((parity + k) % 2) == 0, (sel + k + 1) & 1, st);
         cudaError_t e = cudaStreamEndCapture(c->stream, &gph);
         if (rc) return rc;
         CUDA_TRY(e);
-        CUDA_TRY(cudaGraphInstantiate(&c->graph[start], gph, 0));
+        swe_ctx::Graph g;
+        CUDA_TRY(cudaGraphInstantiate(&g.exec, gph, 0));
         cudaGraphDestroy(gph);
+        g.kernels = c->launches - before;
+        c->launches = before;  // captured, not launched
+        it = c->graphs.emplace(key, g).first;
     }
-    c->graph_kernels = (c->launches - before) / 2;  // our kernels per graph launch
-    c->launches = before;                          // captured, not launched
-    c->graph_len = len;
+    *out = &it->second;
     return SWE_OK;
+}
+
+// Graph chunks for `left` steps: powers of two of at most 64 steps
+// (20 = 16 + 4), so any step count runs from a handful of cached graphs.
+std::vector<int> chunk_plan(uint64_t left) {
+    std::vector<int> v;
+    while (left) {
+        int n = 64;
+        while (static_cast<uint64_t>(n) > left) n >>= 1;
+        v.push_back(n);
+        left -= static_cast<uint64_t>(n);
+    }
+    return v;
 }
 
 }  // namespace
@@ -555,6 +574,9 @@ EXPORT int swe_cuda_create(const swe_grid* grid, const swe_physics* phys, const 
     c->smooth = phys->nu_art > 0.0;  // StepPlan::standard(nu_art > 0), executor.hpp:730
     c->manning = phys->manning_n > 0.0;
     c->R = c->smooth ? 2 : 1;
+    c->halo_x = c->R;
+    if (const char* hx = std::getenv("SWE_DEBUG_HALO_ROWS"))  // test hook (halo mutation)
+        c->halo_x = std::max(0, std::min(c->R, std::atoi(hx)));
     c->j0 = bands[ex.rank].first;
     c->nloc = bands[ex.rank].second - bands[ex.rank].first;
     const int out_w = SWE_TILE_W(c->R);
@@ -696,6 +718,8 @@ EXPORT void swe_cuda_destroy(swe_ctx* c) {
 
 namespace {
 
+constexpr int kNcclSms = 2;  // SMs left free for NCCL kernels on strips
+
 // Guided chunking: the first ~80 % of a launch's rows go out in `chunk`-row
 // items, the rest in quarter-size items, so the dynamic queue ends with short
 // items and the last warps finish together.  SWE_GUIDED=0 keeps uniform chunks.
@@ -807,6 +831,10 @@ int finish_load(swe_ctx* c, double t, swe_status* st) {
     c->occ = swe_step_occupancy(c->exact, v);
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->ex.device);
+    // NCCL strips: leave two SMs to NCCL's send/recv and allreduce kernels so
+    // the halo exchange runs beside the persistent interior launch instead of
+    // after it (its CTAs never retire early)
+    if (c->ex.nranks > 1 && !(c->ex.flags & SWE_EXEC_LOCAL_GROUP)) nsm = std::max(1, nsm - kNcclSms);
     // persistent grid: every resident warp is a worker; small grids keep at
     // least 4 rows per worker so the 2R warm-up rows stay amortised
     const long long units = static_cast<long long>(c->ntiles) * nloc;
@@ -1123,7 +1151,23 @@ EXPORT int swe_cuda_advance_marked(swe_ctx* c, double t_end, double t_mark, uint
     int rc = write_ctl(c, st);
     if (rc) return rc;
     const bool use_graph = !(c->ex.flags & SWE_EXEC_NO_GRAPH) && (!c->tr || c->tr->capturable());
-    const int chunk = 64;
+    // one batch = the chunks covering the steps still to run (64 at a time
+    // when the run is bounded only by t_end / t_mark), launched back to back
+    // without a host sync; launches after a halting step are device no-ops
+    auto batch_of = [&](uint64_t launched) {
+        if (!max_steps) return std::vector<int>{64};
+        return chunk_plan(max_steps - launched);
+    };
+    if (use_graph) {  // build the first batch's graphs before the timed region
+        uint64_t par = h.step_index, sl = static_cast<uint64_t>(h.sel);
+        for (int n : batch_of(0)) {
+            swe_ctx::Graph* g;
+            rc = get_graph(c, n, static_cast<int>(par % 2), static_cast<int>(sl % 2), &g, st);
+            if (rc) return rc;
+            par += n;
+            sl += n;
+        }
+    }
     uint64_t launched = 0;
     unsigned long long committed_before = 0;
     int rc_final = SWE_OK;
@@ -1131,48 +1175,34 @@ EXPORT int swe_cuda_advance_marked(swe_ctx* c, double t_end, double t_mark, uint
     while (true) {
         if (h.done) break;
         if (max_steps && launched >= max_steps) break;
-        const uint64_t left = max_steps ? max_steps - launched : UINT64_MAX;
-        const uint64_t parity = h.step_index;  // next step's parity
-        uint64_t n;
-        if (use_graph && left >= static_cast<uint64_t>(chunk)) {
-            if (c->graph_len != chunk) {
-                rc = build_graphs(c, chunk, st);
+        uint64_t par = h.step_index, sl = static_cast<uint64_t>(h.sel);
+        for (int n : batch_of(launched)) {
+            if (use_graph) {
+                swe_ctx::Graph* g;
+                rc = get_graph(c, n, static_cast<int>(par % 2), static_cast<int>(sl % 2), &g, st);
                 if (rc) return rc;
-            }
-            // graph candidates assume sel = 0 at the chunk start; for sel = 1
-            // the strip halo sends target the other buffer, so strips fall
-            // back to plain launches in that case.
-            if (c->ex.nranks > 1 && h.sel != 0) {
-                for (int k = 0; k < chunk; ++k) {
-                    rc = enqueue_step(c, ((parity + k) % 2) == 0, (h.sel + k + 1) & 1, st);
+                CUDA_TRY(cudaGraphLaunch(g->exec, c->stream));
+                c->launches += g->kernels;
+            } else {
+                for (int k = 0; k < n; ++k) {
+                    rc = enqueue_step(c, ((par + k) % 2) == 0, static_cast<int>((sl + k + 1) & 1), st);
                     if (rc) return rc;
                 }
-            } else {
-                CUDA_TRY(cudaGraphLaunch(c->graph[parity % 2], c->stream));
-                c->launches += c->graph_kernels;
             }
-            n = chunk;
-        } else {
-            n = std::min<uint64_t>(left, static_cast<uint64_t>(chunk));
-            for (uint64_t k = 0; k < n; ++k) {
-                rc = enqueue_step(c, ((parity + k) % 2) == 0, (h.sel + k + 1) & 1, st);
-                if (rc) return rc;
-            }
+            par += n;
+            sl += n;
         }
-        (void)n;
         rc = read_ctl(c, st);
         if (rc) return rc;
         // keep the host mirror of the committed selector/time in sync
         c->sel = h.sel;
         c->t = h.t;
         if (h.status != SWE_OK) {
-            const unsigned long long steps_ok = h.steps_done;
             rc = resolve(c, st);
             c->sel = h.sel;
             c->t = h.t;
             if (rc) {
                 rc_final = rc;
-                (void)steps_ok;
                 break;
             }
             // diagnosis committed the step on the host: continue the run
@@ -1261,4 +1291,17 @@ EXPORT int swe_cuda_activity(swe_ctx* c, swe_activity* out) {
     return SWE_OK;
 }
 EXPORT int32_t swe_cuda_halo_rows(const swe_ctx* c) { return c ? c->R : 0; }
+EXPORT int swe_cuda_state_digest(swe_ctx* c, uint64_t* digest, swe_status* st) {
+    if (!c || !c->loaded) return set_status(st, SWE_ERR_CONFIG, -1, -1, 0, "state_digest: no state loaded");
+    CUDA_TRY(cudaSetDevice(c->ex.device));
+    CUDA_TRY(cudaMemsetAsync(c->d_scan, 0, sizeof(unsigned long long), c->stream));
+    digest_kernel<<<std::max(1, std::min(c->nloc, 148 * 8)), 256, 0, c->stream>>>(
+        c->d_buf[c->sel], c->pitch, c->R, c->g.nx, c->nloc, c->j0, c->d_scan);
+    CUDA_TRY(cudaGetLastError());
+    unsigned long long v = 0;
+    CUDA_TRY(cudaMemcpyAsync(&v, c->d_scan, sizeof v, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    *digest = v;
+    return ok_status(st);
+}
 EXPORT uint64_t swe_cuda_launch_count(const swe_ctx* c) { return c ? c->launches : 0; }

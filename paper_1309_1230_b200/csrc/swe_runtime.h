@@ -7,6 +7,7 @@
 #include <cstdarg>
 #include <cstddef>
 #include <cstring>
+#include <map>
 #include <string>
 
 #include <cuda.h>
@@ -27,6 +28,7 @@ struct swe_ctx {
     swe_boundary_set bnd{};
     swe_exec ex{};
     int R = 1, nloc = 0, j0 = 0, pitch = 0, ntiles = 0;
+    int halo_x = 1;  // committed rows exchanged with each strip neighbour (R; test hook may shrink it)
     bool smooth = false, manning = false, flat = true, xonly = false, loaded = false, exact = true;
     int clamp_any = 0;
     int warnings_total = 0;
@@ -55,9 +57,14 @@ struct swe_ctx {
     StepParams prm{};
     int ncta = 0;
     int occ = 1;
-    cudaGraphExec_t graph[2] = {nullptr, nullptr};
-    int graph_len = 0;
-    unsigned long long graph_kernels = 0;  // our kernels in one captured graph
+    // CUDA graphs of `len` consecutive steps, keyed by (len, parity of the
+    // first step, committed selector at the start -- strips only: the halo
+    // send/recv addresses depend on it); built on first use
+    struct Graph {
+        cudaGraphExec_t exec = nullptr;
+        unsigned long long kernels = 0;  // our kernels per launch of this graph
+    };
+    std::map<int, Graph> graphs;
     swe_rt::Transport* tr = nullptr;  // row-strip collectives (NCCL or local group); null for one rank
     unsigned long long* d_xr = nullptr;  // local-group allreduce scratch
     // strips: halo exchange overlapped with the interior (edge + interior launches)
@@ -121,6 +128,7 @@ __global__ void dry_scan_kernel(const double* b, int P, int R, int nx, int ny, i
                                 double dx, double dy, int fwd, int exact, BcSet bs, const double* z_w,
                                 const double* z_e, const double* z_s, const double* z_n, double h_min,
                                 unsigned long long* out);
+__global__ void digest_kernel(const double* b, int P, int R, int nx, int nloc, int j0, unsigned long long* out);
 __global__ void selftest_div_kernel(const double* a, const double* b, size_t n, int exact, double* out);
 __global__ void max_reduce_kernel(RedPtrs in, int nranks, int n, unsigned long long* out);
 

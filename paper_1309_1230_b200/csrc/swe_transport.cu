@@ -3,6 +3,7 @@
 #include <dlfcn.h>
 
 #include <chrono>
+#include <cstdio>
 #include <condition_variable>
 #include <map>
 #include <mutex>
@@ -68,10 +69,26 @@ NcclApi g_nccl;
                               static_cast<int>(r_), __FILE__, __LINE__);                         \
     } while (0)
 
+// One communicator per (unique id, rank, size, device) and process: every
+// Stepper of a rank built with the same id shares it (the bench and the CLI
+// create several Steppers per run); destroyed with its last user.
+struct CommEntry {
+    ncclComm_t comm = nullptr;
+    int refs = 0;
+};
+std::mutex g_comms_m;
+std::map<std::string, CommEntry> g_comms;
+
 struct NcclTransport final : Transport {
     ncclComm_t comm = nullptr;
+    std::string key;
     ~NcclTransport() override {
-        if (comm && g_nccl.CommDestroy) g_nccl.CommDestroy(comm);
+        std::lock_guard<std::mutex> lk(g_comms_m);
+        auto it = g_comms.find(key);
+        if (it != g_comms.end() && --it->second.refs == 0) {
+            if (it->second.comm && g_nccl.CommDestroy) g_nccl.CommDestroy(it->second.comm);
+            g_comms.erase(it);
+        }
     }
     int allreduce_max(swe_ctx* c, cudaStream_t s, unsigned long long* d, int n, swe_status* st) override;
     int sendrecv(swe_ctx* c, cudaStream_t s, const void* su, void* ru, const void* sd, void* rd, size_t bytes,
@@ -232,9 +249,27 @@ int create_transport(swe_ctx* c, const swe_exec& ex, const void* nccl_id, swe_st
         if (!g_nccl.load(err)) return set_status(st, SWE_ERR_RUNTIME, -1, -1, 0, "%s", err.c_str());
         auto* t = new NcclTransport();
         c->tr = t;
-        ncclUniqueId id;
-        std::memcpy(&id, nccl_id, sizeof id);
-        NCCL_TRY(g_nccl.CommInitRank(&t->comm, ex.nranks, id, ex.rank));
+        t->key.assign(static_cast<const char*>(nccl_id), SWE_NCCL_ID_BYTES);
+        t->key += ":" + std::to_string(ex.rank) + "/" + std::to_string(ex.nranks) + "@" + std::to_string(ex.device);
+        std::lock_guard<std::mutex> lk(g_comms_m);
+        CommEntry& e = g_comms[t->key];
+        if (!e.comm) {
+            ncclUniqueId id;
+            std::memcpy(&id, nccl_id, sizeof id);
+            const ncclResult_t r = g_nccl.CommInitRank(&e.comm, ex.nranks, id, ex.rank);
+            if (r != ncclSuccess) {
+                g_comms.erase(t->key);
+                t->key.clear();
+                return set_status(st, SWE_ERR_RUNTIME, -1, -1, 0.0, "NCCL error %d in ncclCommInitRank",
+                                  static_cast<int>(r));
+            }
+            char bus[32] = "?";
+            cudaDeviceGetPCIBusId(bus, sizeof bus, ex.device);
+            std::fprintf(stderr, "swe-b200: NCCL communicator rank %d of %d on device %d (PCI %s) initialised\n",
+                         ex.rank, ex.nranks, ex.device, bus);
+        }
+        ++e.refs;
+        t->comm = e.comm;
     }
     return SWE_OK;
 }

@@ -395,6 +395,15 @@ class Stepper:
     def halo_rows(self) -> int:
         return self._lib.swe_cuda_halo_rows(self._ctx)
 
+    def state_digest(self) -> int:
+        """This rank's additive digest of the committed state (swe_cuda_state_digest);
+        the whole grid's digest is the sum of the ranks' values mod 2**64."""
+        d = C.c_uint64()
+        st = abi.swe_status()
+        rc = self._lib.swe_cuda_state_digest(self._ctx, C.byref(d), C.byref(st))
+        self._check(rc, st)
+        return d.value
+
 
 def partition_scanlines(ny: int, workers: int):
     """executor.hpp:189-208: contiguous bands, sizes differ by <= 1, larger first."""
