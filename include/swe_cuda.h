@@ -176,7 +176,13 @@ typedef struct swe_activity {
 /* StepTimings-style device counters (executor.hpp:153-172), CUDA-event based */
 typedef struct swe_timing {
     uint64_t steps;
-    double step_seconds;   /* sum of device time of step launches */
+    double step_seconds;      /* sum of device time of step launches (K1-K6 + smoothing run fused) */
+    /* strips, swe_cuda_step only (device events; advance() runs under CUDA
+     * graphs and does not split its time): the halo send/recv, overlapped
+     * with the interior rows, and the reduction-word allreduce */
+    uint64_t exchange_steps;
+    double exchange_seconds;
+    double allreduce_seconds;
 } swe_timing;
 
 typedef struct swe_ctx swe_ctx;

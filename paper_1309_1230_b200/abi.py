@@ -94,7 +94,8 @@ class swe_accounting(C.Structure):
 
 
 class swe_timing(C.Structure):
-    _fields_ = [("steps", C.c_uint64), ("step_seconds", C.c_double)]
+    _fields_ = [("steps", C.c_uint64), ("step_seconds", C.c_double), ("exchange_steps", C.c_uint64),
+                ("exchange_seconds", C.c_double), ("allreduce_seconds", C.c_double)]
 
 
 DP = C.POINTER(C.c_double)

@@ -222,13 +222,17 @@ int enqueue_step(swe_ctx* c, bool fwd, int cand, swe_status* st) {
         CUDA_TRY(cudaEventRecord(c->ev_fork, c->stream));
         CUDA_TRY(cudaStreamWaitEvent(c->stream_edge, c->ev_fork, 0));
         CUDA_TRY(swe_launch_step(c->exact, v, c->ncta_edge, c->stream_edge, c->prm_edge));
+        if (c->time_exchange) CUDA_TRY(cudaEventRecord(c->ev_x[0], c->stream_edge));
         int rc = halo_exchange(c, cand, c->stream_edge, st);
         if (rc) return rc;
+        if (c->time_exchange) CUDA_TRY(cudaEventRecord(c->ev_x[1], c->stream_edge));
         CUDA_TRY(cudaEventRecord(c->ev_join, c->stream_edge));
         CUDA_TRY(swe_launch_step(c->exact, v, c->ncta, c->stream, c->prm_int));
         CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+        if (c->time_exchange) CUDA_TRY(cudaEventRecord(c->ev_x[2], c->stream));
         rc = c->tr->allreduce_max(c, c->stream, c->d_ctl->red, RED_N, st);
         if (rc) return rc;
+        if (c->time_exchange) CUDA_TRY(cudaEventRecord(c->ev_x[3], c->stream));
         CUDA_TRY(swe_launch_finalize(c->stream, c->prm));
         c->launches += 3 + (c->tr->capturable() ? 0 : 1);  // edge + interior + finalize (+ local max kernel)
         return SWE_OK;
@@ -244,10 +248,16 @@ int enqueue_step(swe_ctx* c, bool fwd, int cand, swe_status* st) {
         // allreduce): ranks may take different paths (strip heights differ
         // by one row, early exit depends on the local bed) and NCCL requires
         // every rank to issue a communicator's operations in the same order
+        if (c->time_exchange) CUDA_TRY(cudaEventRecord(c->ev_x[0], c->stream));
         int rc = halo_exchange(c, cand, c->stream, st);
         if (rc) return rc;
+        if (c->time_exchange) {
+            CUDA_TRY(cudaEventRecord(c->ev_x[1], c->stream));
+            CUDA_TRY(cudaEventRecord(c->ev_x[2], c->stream));
+        }
         rc = c->tr->allreduce_max(c, c->stream, c->d_ctl->red, RED_N, st);
         if (rc) return rc;
+        if (c->time_exchange) CUDA_TRY(cudaEventRecord(c->ev_x[3], c->stream));
         CUDA_TRY(swe_launch_finalize(c->stream, c->prm));
         c->launches += 1 + (c->tr->capturable() ? 0 : 1);  // finalize (+ local max kernel)
     }
@@ -593,6 +603,7 @@ EXPORT int swe_cuda_create(const swe_grid* grid, const swe_physics* phys, const 
         CUDA_TRY(cudaStreamCreateWithPriority(&c->stream_edge, cudaStreamNonBlocking, hi));
         CUDA_TRY(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
         CUDA_TRY(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+        for (auto& e : c->ev_x) CUDA_TRY(cudaEventCreate(&e));
     }
     CUDA_TRY(cudaEventCreate(&c->ev0));
     CUDA_TRY(cudaEventCreate(&c->ev1));
@@ -711,6 +722,8 @@ EXPORT void swe_cuda_destroy(swe_ctx* c) {
     if (c->ev1) cudaEventDestroy(c->ev1);
     if (c->stream_edge) cudaStreamDestroy(c->stream_edge);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    for (auto& e : c->ev_x)
+        if (e) cudaEventDestroy(e);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
@@ -1039,7 +1052,9 @@ EXPORT int swe_cuda_step(swe_ctx* c, double dt, uint64_t step_index, double t_af
     int rc = write_ctl(c, st);
     if (rc) return rc;
     CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
+    c->time_exchange = c->ex.nranks > 1;
     rc = enqueue_step(c, fwd, c->sel ^ 1, st);
+    c->time_exchange = false;
     if (rc) return rc;
     CUDA_TRY(cudaEventRecord(c->ev1, c->stream));
     rc = read_ctl(c, st);
@@ -1048,6 +1063,14 @@ EXPORT int swe_cuda_step(swe_ctx* c, double dt, uint64_t step_index, double t_af
     cudaEventElapsedTime(&ms, c->ev0, c->ev1);
     c->timing.steps += 1;
     c->timing.step_seconds += ms * 1e-3;
+    if (c->ex.nranks > 1) {
+        float mx = 0.f, ma = 0.f;
+        cudaEventElapsedTime(&mx, c->ev_x[0], c->ev_x[1]);
+        cudaEventElapsedTime(&ma, c->ev_x[2], c->ev_x[3]);
+        c->timing.exchange_steps += 1;
+        c->timing.exchange_seconds += mx * 1e-3;
+        c->timing.allreduce_seconds += ma * 1e-3;
+    }
     rc = resolve(c, st);
     if (rc) return rc;
     c->sel = h.sel;

@@ -73,6 +73,10 @@ struct swe_ctx {
     int ncta_edge = 0;
     cudaStream_t stream_edge = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // strips, step() only: timing events around the halo send/recv and the
+    // allreduce (recorded when c->time_exchange is set, never under capture)
+    cudaEvent_t ev_x[4] = {nullptr, nullptr, nullptr, nullptr};
+    bool time_exchange = false;
     unsigned long long launches = 0;
     swe_timing timing{};
     double tz_x = 0, tz_y = 0;

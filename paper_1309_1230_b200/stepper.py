@@ -373,6 +373,14 @@ class Stepper:
         self._lib.swe_cuda_timing(self._ctx, C.byref(t))
         return t.steps, t.step_seconds
 
+    def exchange_timing(self) -> dict:
+        """Strips, step() calls only: device time of the halo send/recv
+        (overlapped with the interior rows) and of the allreduce."""
+        t = abi.swe_timing()
+        self._lib.swe_cuda_timing(self._ctx, C.byref(t))
+        return {"steps": t.exchange_steps, "exchange_seconds": t.exchange_seconds,
+                "allreduce_seconds": t.allreduce_seconds}
+
     def accounting(self) -> dict:
         """StepAccounting (executor.hpp:218-222, 804) of this rank, per step."""
         a = abi.swe_accounting()

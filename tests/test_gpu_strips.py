@@ -52,6 +52,7 @@ def run_strips(sc, nranks, exact, steps, early=False, api="advance"):
     states = [None] * nranks
     launches = [0] * nranks
     acc = [None] * nranks
+    xt = [None] * nranks
     errors = []
 
     def worker(r):
@@ -68,6 +69,7 @@ def run_strips(sc, nranks, exact, steps, early=False, api="advance"):
             states[r] = (r0, r1, h, qx, qy, st.time())
             launches[r] = st.launch_count()
             acc[r] = st.accounting()
+            xt[r] = st.exchange_timing()
             st.close()
         except Exception as e:  # surfaced by the caller
             errors.append((r, repr(e)))
@@ -84,6 +86,7 @@ def run_strips(sc, nranks, exact, steps, early=False, api="advance"):
     assert all(x == results[0] for x in results), results  # every rank sees the same outcome
     run_strips.launches = launches
     run_strips.accounting = acc
+    run_strips.exchange = xt
     return fs, results[0]
 
 
@@ -137,6 +140,9 @@ def test_strips_host_step_api():
     ref, rr = run_single(sc, True, 30, api="step")
     got, rg = run_strips(sc, 3, True, 30, api="step")
     assert rr == rg and same(ref, got)
+    # step() times the halo exchange and the allreduce of every strip
+    for x in run_strips.exchange:
+        assert x["steps"] == 30 and x["exchange_seconds"] > 0.0 and x["allreduce_seconds"] > 0.0
 
 
 def test_strips_with_early_exit():
