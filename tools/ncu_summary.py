@@ -37,6 +37,14 @@ lines.append(f"  duration {t_s * 1e3:.3f} ms -> algorithmic {alg / t_s:.0f} GB/s
 warp_inst = num("smsp__inst_executed.sum")
 if warp_inst:
     lines.append(f"  thread instructions per cell: {warp_inst * 32 / cells:.1f}")
+stalls = {k[len("smsp__pcsamp_warps_issue_stalled_"):]: num(k) for k in m
+          if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("_not_issued")}
+stalls = {k: v for k, v in stalls.items() if v}
+if stalls:
+    tot = sum(stalls.values())
+    lines.append("warp-state samples (smsp__pcsamp_warps_issue_stalled_*, share of all samples):")
+    for k, v in sorted(stalls.items(), key=lambda kv: -kv[1])[:10]:
+        lines.append(f"  {k:28s}{100 * v / tot:5.1f}%")
 open(out, "w").write("\n".join(lines) + "\n")
 print("\n".join(lines))
 print(json.dumps({"traffic_GB_per_launch": rd + wr}))
