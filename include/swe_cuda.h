@@ -272,6 +272,10 @@ int swe_cuda_state_digest(swe_ctx* ctx, uint64_t* digest, swe_status* st);
 int swe_cuda_nccl_unique_id(void* out, swe_status* st);
 
 /* ---- diagnostics ----------------------------------------------------- */
+/* SWE_CHECKED builds only (tools/checked_run.sh): counts corrupted bytes in
+ * the guard bands around every live device allocation of the library; the
+ * product build returns SWE_ERR_CONFIG. */
+int swe_cuda_debug_guard_check(uint64_t* corrupted_bytes, uint64_t* allocations, swe_status* st);
 /* Runs the step kernel's shared-reciprocal division on device arrays copied
  * from the host: out[k] = a[k] / b[k] as the step computes it (exact != 0:
  * SWE_EXEC_EXACT arithmetic, else the fast-mode quotient).  Used by the

@@ -126,6 +126,7 @@ SIGNATURES = {
     "swe_cuda_rows": (None, [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "swe_cuda_halo_rows": (C.c_int32, [C.c_void_p]),
     "swe_cuda_state_digest": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(swe_status)]),
+    "swe_cuda_debug_guard_check": (C.c_int, [C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(swe_status)]),
     "swe_cuda_nccl_unique_id": (C.c_int, [C.c_void_p, ST]),
     "swe_cuda_version": (C.c_char_p, []),
     "swe_cuda_launch_count": (C.c_uint64, [C.c_void_p]),

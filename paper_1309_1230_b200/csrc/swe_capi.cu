@@ -12,6 +12,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -48,6 +50,43 @@ int ok_status(swe_status* st) {
 }  // namespace swe_rt
 
 namespace swe_rt {
+
+// ---------------------------------------------------------------- device allocations
+// Product build: cudaMalloc / cudaFree.  SWE_CHECKED build: every allocation
+// gets 64 KiB guard bands of a fixed byte pattern on both sides;
+// swe_cuda_debug_guard_check() reports corrupted guard bytes (a stray write
+// past any buffer the kernels touch).
+#if SWE_CHECKED
+namespace {
+constexpr size_t kGuard = 64 * 1024;
+constexpr unsigned char kGuardByte = 0xA5;
+std::mutex g_alloc_m;
+std::map<void*, std::pair<char*, size_t>> g_allocs;  // user pointer -> (base, user bytes)
+}  // namespace
+cudaError_t dev_alloc(void** p, size_t bytes) {
+    char* base = nullptr;
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&base), bytes + 2 * kGuard);
+    if (e != cudaSuccess) return e;
+    e = cudaMemset(base, kGuardByte, kGuard);
+    if (e == cudaSuccess) e = cudaMemset(base + kGuard + bytes, kGuardByte, kGuard);
+    if (e != cudaSuccess) return e;
+    *p = base + kGuard;
+    std::lock_guard<std::mutex> lk(g_alloc_m);
+    g_allocs[*p] = {base, bytes};
+    return cudaSuccess;
+}
+void dev_free(void* p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_alloc_m);
+    auto it = g_allocs.find(p);
+    if (it == g_allocs.end()) return;
+    cudaFree(it->second.first);
+    g_allocs.erase(it);
+}
+#else
+cudaError_t dev_alloc(void** p, size_t bytes) { return cudaMalloc(p, bytes); }
+void dev_free(void* p) { cudaFree(p); }
+#endif
 
 // ---------------------------------------------------------------- TMA descriptors
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -608,25 +647,25 @@ EXPORT int swe_cuda_create(const swe_grid* grid, const swe_physics* phys, const 
     CUDA_TRY(cudaEventCreate(&c->ev0));
     CUDA_TRY(cudaEventCreate(&c->ev1));
     for (int k = 0; k < 2; ++k) {
-        CUDA_TRY(cudaMalloc(&c->d_buf[k], c->buf_doubles * sizeof(double)));
+        CUDA_TRY(dev_alloc(reinterpret_cast<void**>(&c->d_buf[k]), c->buf_doubles * sizeof(double)));
         fill_benign_kernel<<<148 * 8, 256, 0, c->stream>>>(c->d_buf[k], rows * 3, c->pitch);
         CUDA_TRY(cudaGetLastError());
     }
     const size_t zrows = rows;
-    CUDA_TRY(cudaMalloc(&c->d_zw, zrows * sizeof(double)));
-    CUDA_TRY(cudaMalloc(&c->d_ze, zrows * sizeof(double)));
-    CUDA_TRY(cudaMalloc(&c->d_zs, grid->nx * sizeof(double)));
-    CUDA_TRY(cudaMalloc(&c->d_zn, grid->nx * sizeof(double)));
-    CUDA_TRY(cudaMalloc(&c->d_zp, static_cast<size_t>(c->nloc + 2 * c->R + 2) * grid->nx * sizeof(double)));
+    CUDA_TRY(dev_alloc(reinterpret_cast<void**>(&c->d_zw), zrows * sizeof(double)));
+    CUDA_TRY(dev_alloc(reinterpret_cast<void**>(&c->d_ze), zrows * sizeof(double)));
+    CUDA_TRY(dev_alloc(reinterpret_cast<void**>(&c->d_zs), grid->nx * sizeof(double)));
+    CUDA_TRY(dev_alloc(reinterpret_cast<void**>(&c->d_zn), grid->nx * sizeof(double)));
+    CUDA_TRY(dev_alloc(reinterpret_cast<void**>(&c->d_zp), static_cast<size_t>(c->nloc + 2 * c->R + 2) * grid->nx * sizeof(double)));
     CUDA_TRY(cudaMemsetAsync(c->d_zw, 0, zrows * sizeof(double), c->stream));
     CUDA_TRY(cudaMemsetAsync(c->d_ze, 0, zrows * sizeof(double), c->stream));
     CUDA_TRY(cudaMemsetAsync(c->d_zs, 0, grid->nx * sizeof(double), c->stream));
     CUDA_TRY(cudaMemsetAsync(c->d_zn, 0, grid->nx * sizeof(double), c->stream));
-    CUDA_TRY(cudaMalloc(&c->d_scan, SCAN_N * sizeof(unsigned long long)));
-    CUDA_TRY(cudaMalloc(&c->d_flags, 4 * sizeof(unsigned)));
-    CUDA_TRY(cudaMalloc(&c->d_stats, 4 * sizeof(unsigned long long)));
+    CUDA_TRY(dev_alloc(reinterpret_cast<void**>(&c->d_scan), SCAN_N * sizeof(unsigned long long)));
+    CUDA_TRY(dev_alloc(reinterpret_cast<void**>(&c->d_flags), 4 * sizeof(unsigned)));
+    CUDA_TRY(dev_alloc(reinterpret_cast<void**>(&c->d_stats), 4 * sizeof(unsigned long long)));
     CUDA_TRY(cudaMemsetAsync(c->d_stats, 0, 4 * sizeof(unsigned long long), c->stream));
-    CUDA_TRY(cudaMalloc(&c->d_ctl, sizeof(SweCtl)));
+    CUDA_TRY(dev_alloc(reinterpret_cast<void**>(&c->d_ctl), sizeof(SweCtl)));
     CUDA_TRY(cudaMallocHost(&c->h_ctl, sizeof(SweCtl)));
     std::memset(c->h_ctl, 0, sizeof(SweCtl));
     CUDA_TRY(cudaMemcpyAsync(c->d_ctl, c->h_ctl, sizeof(SweCtl), cudaMemcpyHostToDevice, c->stream));
@@ -634,7 +673,7 @@ EXPORT int swe_cuda_create(const swe_grid* grid, const swe_physics* phys, const 
     if (ex.nranks > 1) {
         if (!exec->nccl_id)
             return set_status(st, SWE_ERR_CONFIG, -1, -1, 0, "exec: nranks > 1 requires nccl_id");
-        CUDA_TRY(cudaMalloc(&c->d_xr, 16 * sizeof(unsigned long long)));
+        CUDA_TRY(dev_alloc(reinterpret_cast<void**>(&c->d_xr), 16 * sizeof(unsigned long long)));
         const int trc = create_transport(c, ex, exec->nccl_id, st);
         if (trc) return trc;
     }
@@ -668,6 +707,7 @@ EXPORT int swe_cuda_create(const swe_grid* grid, const swe_physics* phys, const 
     p.nloc = c->nloc;
     p.j0 = c->j0;
     p.pitch = c->pitch;
+    p.buf_doubles = static_cast<long long>(c->buf_doubles);
     p.ntiles = c->ntiles;
     p.finalize = ex.nranks > 1 ? 0 : 1;
     p.nranks = ex.nranks;
@@ -700,23 +740,23 @@ EXPORT void swe_cuda_destroy(swe_ctx* c) {
     if (c->stream_edge) cudaStreamSynchronize(c->stream_edge);
     destroy_graphs(c);
     delete c->tr;
-    cudaFree(c->d_xr);
+    dev_free(c->d_xr);
     for (auto& b : c->d_buf)
-        if (b) cudaFree(b);
-    cudaFree(c->d_slope);
-    cudaFree(c->d_zw);
-    cudaFree(c->d_zp);
-    cudaFree(c->d_ze);
-    cudaFree(c->d_zs);
-    cudaFree(c->d_zn);
-    cudaFree(c->d_scan);
-    cudaFree(c->d_flags);
-    cudaFree(c->d_stats);
-    cudaFree(c->d_qflag);
-    cudaFree(c->d_elig);
-    cudaFree(c->d_iflat);
-    cudaFree(c->d_active);
-    cudaFree(c->d_ctl);
+        if (b) dev_free(b);
+    dev_free(c->d_slope);
+    dev_free(c->d_zw);
+    dev_free(c->d_zp);
+    dev_free(c->d_ze);
+    dev_free(c->d_zs);
+    dev_free(c->d_zn);
+    dev_free(c->d_scan);
+    dev_free(c->d_flags);
+    dev_free(c->d_stats);
+    dev_free(c->d_qflag);
+    dev_free(c->d_elig);
+    dev_free(c->d_iflat);
+    dev_free(c->d_active);
+    dev_free(c->d_ctl);
     if (c->h_ctl) cudaFreeHost(c->h_ctl);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
@@ -782,7 +822,7 @@ int finish_load(swe_ctx* c, double t, swe_status* st) {
                                  c->stream));
 
     // slopes + flat-bed detection
-    if (!c->d_slope) CUDA_TRY(cudaMalloc(&c->d_slope, static_cast<size_t>(nloc + 2 * R) * 2 * P * sizeof(double)));
+    if (!c->d_slope) CUDA_TRY(dev_alloc(reinterpret_cast<void**>(&c->d_slope), static_cast<size_t>(nloc + 2 * R) * 2 * P * sizeof(double)));
     CUDA_TRY(cudaMemsetAsync(c->d_slope, 0, static_cast<size_t>(nloc + 2 * R) * 2 * P * sizeof(double), c->stream));
     CUDA_TRY(cudaMemsetAsync(c->d_flags, 0, 4 * sizeof(unsigned), c->stream));
     slopes_kernel<<<std::min(nloc + 2 * R, 148 * 8), 256, 0, c->stream>>>(
@@ -891,17 +931,17 @@ int finish_load(swe_ctx* c, double t, swe_status* st) {
     if (c->early && c->flat) {  // early-exit kernels exist for a flat bed only
         const int nitems = c->ntiles * c->prm.nchunks;
         if (nitems != c->nitems_alloc) {
-            cudaFree(c->d_qflag);
-            cudaFree(c->d_elig);
-            cudaFree(c->d_iflat);
-            cudaFree(c->d_active);
+            dev_free(c->d_qflag);
+            dev_free(c->d_elig);
+            dev_free(c->d_iflat);
+            dev_free(c->d_active);
             c->d_qflag = nullptr;
             c->d_elig = c->d_iflat = nullptr;
             c->d_active = nullptr;
-            CUDA_TRY(cudaMalloc(&c->d_active, static_cast<size_t>(nitems) * sizeof(unsigned)));
-            CUDA_TRY(cudaMalloc(&c->d_qflag, 2 * static_cast<size_t>(nitems) * sizeof(unsigned long long)));
-            CUDA_TRY(cudaMalloc(&c->d_elig, nitems));
-            CUDA_TRY(cudaMalloc(&c->d_iflat, nitems));
+            CUDA_TRY(dev_alloc(reinterpret_cast<void**>(&c->d_active), static_cast<size_t>(nitems) * sizeof(unsigned)));
+            CUDA_TRY(dev_alloc(reinterpret_cast<void**>(&c->d_qflag), 2 * static_cast<size_t>(nitems) * sizeof(unsigned long long)));
+            CUDA_TRY(dev_alloc(reinterpret_cast<void**>(&c->d_elig), nitems));
+            CUDA_TRY(dev_alloc(reinterpret_cast<void**>(&c->d_iflat), nitems));
             c->nitems_alloc = nitems;
         }
         CUDA_TRY(cudaMemsetAsync(c->d_qflag, 0, 2 * static_cast<size_t>(nitems) * sizeof(unsigned long long),
@@ -1272,6 +1312,28 @@ EXPORT int swe_cuda_selftest_div(const double* a, const double* b, size_t n, int
     cudaFree(db);
     cudaFree(dout);
     return ok_status(st);
+}
+
+EXPORT int swe_cuda_debug_guard_check(uint64_t* corrupted_bytes, uint64_t* allocations, swe_status* st) {
+#if SWE_CHECKED
+    std::vector<unsigned char> g(kGuard);
+    uint64_t bad = 0;
+    std::lock_guard<std::mutex> lk(g_alloc_m);
+    for (auto& kv : g_allocs) {
+        char* base = kv.second.first;
+        for (char* band : {base, base + kGuard + kv.second.second}) {
+            CUDA_TRY(cudaMemcpy(g.data(), band, kGuard, cudaMemcpyDeviceToHost));
+            for (unsigned char b : g) bad += (b != kGuardByte);
+        }
+    }
+    *corrupted_bytes = bad;
+    *allocations = g_allocs.size();
+    return ok_status(st);
+#else
+    (void)corrupted_bytes;
+    (void)allocations;
+    return set_status(st, SWE_ERR_CONFIG, -1, -1, 0, "debug_guard_check: library built without SWE_CHECKED");
+#endif
 }
 
 EXPORT double swe_cuda_time(const swe_ctx* c) { return c ? c->t : 0.0; }

@@ -136,6 +136,11 @@ __global__ void digest_kernel(const double* b, int P, int R, int nx, int nloc, i
 __global__ void selftest_div_kernel(const double* a, const double* b, size_t n, int exact, double* out);
 __global__ void max_reduce_kernel(RedPtrs in, int nranks, int n, unsigned long long* out);
 
+// ---------------------------------------------------------------- device allocations (swe_capi.cu)
+// cudaMalloc / cudaFree, with guard bands in SWE_CHECKED builds
+cudaError_t dev_alloc(void** p, size_t bytes);
+void dev_free(void* p);
+
 // ---------------------------------------------------------------- TMA descriptors (swe_capi.cu)
 // 2D map over field_rows rows of P doubles at row_stride doubles (P if 0); box
 // box_cols x box_rows

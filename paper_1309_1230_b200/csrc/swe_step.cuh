@@ -342,6 +342,7 @@ struct Marcher {
             return;
         }
         if constexpr (EARLY) item = p.active[item];
+        SWE_DCHECK(item < static_cast<unsigned>(p.ntiles) * static_cast<unsigned>(p.nchunks));
         const int rc = static_cast<int>(item / p.ntiles);   // row-chunk major: neighbouring
         const int tile = static_cast<int>(item % p.ntiles); // windows share halo sectors in L2
         Seg sg;
@@ -356,6 +357,7 @@ struct Marcher {
             sg.ra = p.row_lo + p.tier_rc * p.chunk + (rc - p.tier_rc) * p.chunk2;
             sg.rb = min(sg.ra + p.chunk2, p.row_hi);
         }
+        SWE_DCHECK(sg.tile >= 0 && sg.tile < p.ntiles && sg.ra >= p.row_lo && sg.ra < sg.rb && sg.rb <= p.row_hi);
         segq[qtail % QN] = sg;
         ++qtail;
         pleft = ((sg.rb - sg.ra) + 2 * R + G - 1) / G;
@@ -368,6 +370,9 @@ struct Marcher {
             if (pleft == 0 && !(pdone || qtail - qhead >= QN - 1)) prod_seg();
             if (pleft == 0) return;
             const int d = pn % D;
+            // the box may run past the buffer at a strip end (TMA fills zeros there,
+            // never consumed), but it must overlap it
+            SWE_DCHECK(px >= 0 && px + 32 <= P && py + G > 0 && py < p.nloc + 2 * R);
             if (lane == 0) {
                 mbar_expect_tx(&bars[d], SLOT * 8);
                 tma_load_2d(stage + d * SLOT, &p.tmap_state[sel], px, py * 3, &bars[d]);
@@ -383,6 +388,7 @@ struct Marcher {
     // segments; the group row of each march iteration is static (see march()).
     template <int GI>
     __device__ __forceinline__ void consume(CellVec& u, double& zx, double& zy) {
+        SWE_DCHECK(ring.d >= 0 && ring.d < D && req < pn);
         if constexpr (GI == 0) mbar_wait(&bars[ring.d], ring.ph);
         constexpr int g = FWD ? GI : G - 1 - GI;  // row within the box (boxes ascend in y)
         const double* st = stage + ring.d * SLOT;
@@ -461,6 +467,8 @@ struct Marcher {
         }
         double* row = orow;  // == nxt + (rr + R) * 3P + (i + R)
         orow += S * 3 * P;
+        SWE_DCHECK(!on || (row == nxt + (static_cast<long long>(rr + R) * 3 * P + (i + R)) && rr >= 0 && rr < p.nloc &&
+                           i >= 0 && i < p.nx));
         if (on && !(SWE_ABL & 1)) {
             row[0] = o.h;
             row[P] = o.qx;
@@ -469,6 +477,7 @@ struct Marcher {
         if constexpr (!EDGE) return;
         if (!on) return;
         if (!(xedge || jj == 0 || jj == p.ny - 1)) return;
+        SWE_DCHECK(row - nxt >= 3 * P && row - nxt + 2 * P + 1 < p.buf_doubles - 3 * P && rr + R < p.nloc + 2 * R);
         if (i == 0) {
             const CellVec g = edge_ghost(SWE_EDGE_W, p.bc[SWE_EDGE_W], o, p.z_w[rr + R], p.h_min);
             row[-1] = g.h;
@@ -872,6 +881,7 @@ struct Marcher {
             const double H = __longlong_as_double(static_cast<long long>(ref));
             const bool quiet = __all_sync(FULL, ok) && H >= p.h_min && finite_d(H);
             if (lane == 0)
+                SWE_DCHECK((sg.ra / p.chunk) * p.ntiles + sg.tile < p.ntiles * p.nchunks);
                 p.qflag[sel ^ 1][(sg.ra / p.chunk) * p.ntiles + sg.tile] = quiet ? ref : 0ull;
         }
     }

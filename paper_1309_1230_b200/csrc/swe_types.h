@@ -90,6 +90,7 @@ struct StepParams {
     int nx, ny;            // global grid
     int nloc, j0;          // rows owned by this rank: global [j0, j0+nloc)
     int pitch;             // doubles per field row (P)
+    long long buf_doubles; // doubles per state buffer (SWE_CHECKED bounds)
     int ntiles;            // x tiles
     int ncta;              // CTAs launched
     int chunk;             // rows per dynamic work item
