@@ -135,7 +135,7 @@ def test_cli_fast_mode_within_tolerance(tmp_path):
     fa, _, ea = sio.parse_snapshot((a / "drops64_final.sws").read_bytes())
     fb, _, eb = sio.parse_snapshot((b / "drops64_final.sws").read_bytes())
     assert ea["step_index"] == eb["step_index"]
-    assert np.abs(fa.h - fb.h).max() <= 1e-10 and np.abs(fa.qx - fb.qx).max() <= 1e-10
+    assert np.abs(fa.h - fb.h).max() <= 1e-12 and np.abs(fa.qx - fb.qx).max() <= 1e-12
 
 
 def test_cli_set_override_and_error_exit_codes(tmp_path):
