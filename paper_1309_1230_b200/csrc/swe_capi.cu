@@ -855,6 +855,14 @@ int finish_load(swe_ctx* c, double t, swe_status* st) {
                 return set_status(st, SWE_ERR_RUNTIME, -1, -1, 0, "%s", err.c_str());
         if (!encode_rows(&c->prm.tmap_slope, c->d_slope, P, static_cast<long long>(nloc + 2 * R) * 2, 2 * G, err))
             return set_status(st, SWE_ERR_RUNTIME, -1, -1, 0, "%s", err.c_str());
+        // TMA-store epilogue: inner extent R + nx (the window's out-of-domain
+        // columns are clipped), rows 3*(nloc+2R), pitch P
+        const int TW = SWE_TILE_W(R);
+        for (int k = 0; k < 2; ++k) {
+            if (!encode_rows(&c->prm.tmap_out[k], c->d_buf[k], R + nx, static_cast<long long>(nloc + 2 * R) * 3, 3 * G,
+                             err, TW, P))
+                return set_status(st, SWE_ERR_RUNTIME, -1, -1, 0, "%s", err.c_str());
+        }
         if (!encode_rows(&c->prm.tmap_slopex, c->d_slope, P, static_cast<long long>(nloc + 2 * R), G, err, 32, 2 * P))
             return set_status(st, SWE_ERR_RUNTIME, -1, -1, 0, "%s", err.c_str());
     }

@@ -52,7 +52,38 @@ constexpr int step_min_blocks() {
 // occupancy (3 stages, 2 for 16 warps on a sloped bed).
 template <bool EXACT, bool FLAT, bool MANNING, bool EARLY>
 constexpr int step_stages() {
+#ifdef SWE_STAGES
+    return SWE_STAGES;
+#else
     return swe_row_group(EXACT, EARLY) == 2 ? 4 : (FLAT || step_min_blocks<EXACT, FLAT, MANNING>() == 3) ? 3 : 2;
+#endif
+}
+
+// Output staging for a TMA-store epilogue: per warp two buffers of one row
+// group ([3G field rows][TW doubles], padded to 128 B), for the variants whose
+// ring + staging fit the SM's 228 KB at their occupancy.  OFF: a TMA tensor
+// store must start on a 16-byte-aligned inner coordinate
+// (tools/tma_store_probe.cu: an odd double offset is an illegal instruction),
+// and with R = 1 the output columns of every window start at an odd padded
+// column; enabling it needs an even column offset for the windows (padding
+// 2 instead of R and a 34-wide load box).  The coalesced STG epilogue is used.
+#ifndef SWE_TMA_STORE
+#define SWE_TMA_STORE 0
+#endif
+template <bool EXACT, bool EARLY, int TW>
+constexpr int step_stage_doubles() {
+    return ((3 * swe_row_group(EXACT, EARLY) * TW * 8 + 127) / 128) * 128 / 8;
+}
+template <int WPB, bool SMOOTH, int BED, bool EXACT, bool MANNING, bool EARLY>
+constexpr bool step_tma_store() {
+    constexpr int NF = BED == 0 ? 3 : BED == 2 ? 4 : 5;
+    constexpr int G = swe_row_group(EXACT, EARLY);
+    constexpr int D = step_stages<EXACT, BED == 0, MANNING, EARLY>();
+    constexpr int TW = SMOOTH ? 28 : 30;
+    constexpr long ring = static_cast<long>(D) * NF * G * 32 * 8;
+    constexpr long stage = 2L * step_stage_doubles<EXACT, EARLY, TW>() * 8;
+    constexpr long per_cta = WPB * (ring + stage + D * 8) + 1536;  // + static smem and the per-CTA reserve
+    return SWE_TMA_STORE != 0 && per_cta * step_min_blocks<EXACT, BED == 0, MANNING>() <= 228L * 1024;
 }
 
 // ---------------------------------------------------------------- PTX helpers
@@ -98,6 +129,21 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
             "r"(smem_u32(dst)),
         "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
         : "memory");
+}
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int x, int y, const void* src) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(map), "r"(x),
+                 "r"(y), "r"(smem_u32(src))
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 // Rows per TMA request (swe_row_group): one 2D box carries G consecutive rows
@@ -272,6 +318,8 @@ struct Marcher {
     static constexpr int SLOT = NF * G * 32;  // doubles per ring slot: [G][3][32] state, [G][2][32] slopes
     static constexpr int TW = 32 - 2 * R;
     static constexpr unsigned FULL = 0xffffffffu;
+    static constexpr bool TSTORE = step_tma_store<WPB, SMOOTH, BED, EXACT, MANNING, EARLY>();
+    static constexpr int SD = step_stage_doubles<EXACT, EARLY, TW>();  // doubles per staging buffer
 
     const StepParams& p;
     double* stage;
@@ -295,7 +343,13 @@ struct Marcher {
     // per-segment constants
     int i, L, r_start;
     bool in_x, out_x, star_ok, xedge;
-    double* orow;  // output row of the next emit (this lane's column)
+    double* orow;  // output row of the next emit (this lane's column; STG epilogue)
+    // TMA-store epilogue: this warp's two staging buffers, groups issued so
+    // far (parity = buffer), the current segment's tile, first output row in
+    // march order and completed groups
+    double* sstage;
+    unsigned sgrp;
+    int seg_tile, erow0, egrp;
     // reductions
     double mx, my;
     int e2;
@@ -418,9 +472,10 @@ struct Marcher {
     }
 
     // output cell: guard (K5), CFL (K6), store, ghosts for the next step (K1)
-    template <bool EDGE>
     // on = false (SWE_EMIT_MASKED, lanes outside the output columns): the
-    // arithmetic runs, the reductions and stores are masked
+    // arithmetic runs, the reductions and stores are masked.  SLOT: the row's
+    // position in its output group (TMA-store epilogue; -1 = STG)
+    template <bool EDGE, int SLOT = -1>
     __device__ __forceinline__ void emit(const CellVec& o, int rr, bool on = true) {
         const int jj = p.j0 + rr;
         double sx, sy;  // executor.hpp:560-580
@@ -465,11 +520,20 @@ struct Marcher {
             qo |= hb | mom;
             qn &= hb & ~mom;
         }
+        if constexpr (TSTORE && SLOT >= 0) {  // stage the row for the warp's TMA store of its group
+            constexpr int gr = FWD ? SLOT : G - 1 - SLOT;  // row within the box (boxes ascend in y)
+            double* sb = sstage + (sgrp & 1u) * SD + gr * 3 * TW + (lane - R);
+            if (on && !(SWE_ABL & 1)) {
+                sb[0] = o.h;
+                sb[TW] = o.qx;
+                sb[2 * TW] = o.qy;
+            }
+        }
         double* row = orow;  // == nxt + (rr + R) * 3P + (i + R)
         orow += S * 3 * P;
         SWE_DCHECK(!on || (row == nxt + (static_cast<long long>(rr + R) * 3 * P + (i + R)) && rr >= 0 && rr < p.nloc &&
                            i >= 0 && i < p.nx));
-        if (on && !(SWE_ABL & 1)) {
+        if (!(TSTORE && SLOT >= 0) && on && !(SWE_ABL & 1)) {
             row[0] = o.h;
             row[P] = o.qx;
             row[2 * P] = o.qy;
@@ -504,6 +568,29 @@ struct Marcher {
             gr[P] = g.qx;
             gr[2 * P] = g.qy;
         }
+    }
+
+    // TMA-store epilogue, warp-uniform: before the first row of a group is
+    // staged, the store issued from the same buffer two groups ago must have
+    // finished reading it; after the last row, every lane's staged values are
+    // made visible to the async proxy and lane 0 stores the group's box
+    // (G rows x h/qx/qy x TW columns; the tensor map ends at column R + nx, so
+    // the last window's out-of-domain lanes are clipped).
+    __device__ __forceinline__ void group_begin() {
+        if (lane == 0) bulk_wait_read<1>();
+        __syncwarp();
+    }
+    __device__ __forceinline__ void group_flush() {
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+            const int y0 = FWD ? erow0 + egrp * G : erow0 - (egrp + 1) * G;  // lowest row of the group
+            SWE_DCHECK(y0 >= 0 && y0 + G <= p.nloc);
+            tma_store_2d(&p.tmap_out[sel ^ 1], seg_tile * TW + R, (y0 + R) * 3, sstage + (sgrp & 1u) * SD);
+            bulk_commit();
+        }
+        ++sgrp;
+        ++egrp;
     }
 
     // boundary faces of row b (executor.hpp:471-514): walls carry pressure only,
@@ -613,9 +700,10 @@ struct Marcher {
     // One iteration k of the march: `in` -> `out`.
     // EDGE = false: the segment touches no domain edge (interior window, rows
     // clear of j = 0 and j = ny-1), so every boundary test is compiled out.
-    template <bool EDGE, bool DO12, bool DO3, bool EMIT, int GI = 0>
+    template <bool EDGE, bool DO12, bool DO3, bool EMIT, int GI = 0, int SLOT = -1>
     __device__ __forceinline__ void iter(int k, const Carry& in, Carry& out) {
         const int b = r_start + S * k;  // stage-2 row (local)
+        if constexpr (TSTORE && EMIT && SLOT == 0) group_begin();
         if constexpr (DO12) {
             // ======== stage 1: committed row b+S
             consume<GI>(out.U, out.zx, out.zy);
@@ -806,9 +894,9 @@ struct Marcher {
             const int c_row = b;
             if constexpr (!SMOOTH) {
                 if constexpr (SWE_EMIT_MASKED) {
-                    if (EMIT) emit<EDGE>(C, c_row, out_x);
+                    if (EMIT) emit<EDGE, SLOT>(C, c_row, out_x);
                 } else {
-                    if (EMIT && out_x) emit<EDGE>(C, c_row);
+                    if (EMIT && out_x) emit<EDGE, SLOT>(C, c_row);
                 }
             } else {
                 // smoothing of row q = c - S   (executor.hpp:533-540, scheme.hpp:197-204)
@@ -840,13 +928,14 @@ struct Marcher {
                             o.qx = __fma_rn(nu, __fma_rn(-4.0, Cp.qx, (ce.qx + cw.qx) + (cn.qx + cs.qx)), Cp.qx);
                             o.qy = __fma_rn(nu, __fma_rn(-4.0, Cp.qy, (ce.qy + cw.qy) + (cn.qy + cs.qy)), Cp.qy);
                         }
-                        emit<EDGE>(o, q);
+                        emit<EDGE, SLOT>(o, q);
                     }
                 }
                 out.Cpp = Cp;
                 out.Cp = C;
             }
         }
+        if constexpr (TSTORE && EMIT && SLOT == G - 1) group_flush();
     }
 
     // March one segment: output rows [ra, rb) of one 32-column window.
@@ -859,6 +948,9 @@ struct Marcher {
         star_ok = FWD ? (lane < 31) : (lane > 0);
         xedge = (xw0 <= 0) || (xw0 + 31 >= p.nx - 1);
         r_start = FWD ? sg.ra : sg.rb - 1;
+        seg_tile = sg.tile;
+        erow0 = FWD ? sg.ra : sg.rb;
+        egrp = 0;
 
         orow = nxt + static_cast<size_t>(r_start + R) * 3 * P + (i + R);  // first output row
         qo = 0ull;
@@ -880,9 +972,10 @@ struct Marcher {
             const bool ok = !out_x || (qo == qn && qo == ref);
             const double H = __longlong_as_double(static_cast<long long>(ref));
             const bool quiet = __all_sync(FULL, ok) && H >= p.h_min && finite_d(H);
-            if (lane == 0)
+            if (lane == 0) {
                 SWE_DCHECK((sg.ra / p.chunk) * p.ntiles + sg.tile < p.ntiles * p.nchunks);
                 p.qflag[sel ^ 1][(sg.ra / p.chunk) * p.ntiles + sg.tile] = quiet ? ref : 0ull;
+            }
         }
     }
 
@@ -917,15 +1010,15 @@ struct Marcher {
         const int k_first = k;
         // carries enter the steady state in B and alternate (B->A, A->B, ...)
         for (; k + G - 1 <= k_last; k += G) {
-            iter<EDGE, true, true, true, (GI0 + 0) % G>(k, B, A);
-            iter<EDGE, true, true, true, (GI0 + 1) % G>(k + 1, A, B);
+            iter<EDGE, true, true, true, (GI0 + 0) % G, 0>(k, B, A);
+            iter<EDGE, true, true, true, (GI0 + 1) % G, 1>(k + 1, A, B);
             if constexpr (G == 4) {
-                iter<EDGE, true, true, true, (GI0 + 2) % G>(k + 2, B, A);
-                iter<EDGE, true, true, true, (GI0 + 3) % G>(k + 3, A, B);
+                iter<EDGE, true, true, true, (GI0 + 2) % G, 2>(k + 2, B, A);
+                iter<EDGE, true, true, true, (GI0 + 3) % G, 3>(k + 3, A, B);
             }
         }
         const int rem = k_last - k + 1;  // 0 .. G-1 tail iterations
-        if (rem > 0) {
+        if (rem > 0) {  // a segment's partial last group: plain STG stores
             iter<EDGE, true, true, true, (GI0 + 0) % G>(k, B, A);
             if constexpr (G == 4) {
                 if (rem > 1) {
@@ -960,6 +1053,9 @@ __global__ void __launch_bounds__(WPB * 32, (step_min_blocks<EXACT, BED == 0, MA
     double* stage = reinterpret_cast<double*>(smem_raw) + warp * (D * M::SLOT);  // [D][SLOT]
     unsigned long long* bars =
         reinterpret_cast<unsigned long long*>(reinterpret_cast<double*>(smem_raw) + WPB * D * M::SLOT) + warp * D;
+    // TMA-store staging: after the rings and barriers, 128-byte aligned
+    constexpr size_t kStageOff = (static_cast<size_t>(WPB) * D * M::SLOT * 8 + WPB * D * 8 + 127) / 128 * 128;
+    double* sstage = reinterpret_cast<double*>(smem_raw + kStageOff) + warp * 2 * M::SD;
 
     if (tid == 0) {
         const volatile SweCtl* vc = ctl;
@@ -1026,11 +1122,17 @@ __global__ void __launch_bounds__(WPB * 32, (step_min_blocks<EXACT, BED == 0, MA
     m.qn = ~0ull;
     m.pend = {1.0, 0.0, 0.0};
     m.pvalid = false;
+    m.sstage = sstage;
+    m.sgrp = 0u;
     m.produce();
     while (m.qhead < m.qtail) {  // the producer keeps the queue ahead of the consumer
         const Seg sg = m.segq[m.qhead % M::QN];
         ++m.qhead;
         m.segment(sg);
+    }
+    if constexpr (M::TSTORE) {  // this warp's bulk stores complete before the step is finalized
+        if (lane == 0) bulk_wait_all();
+        __syncwarp();
     }
 
     // ---- CTA reduction of the CFL maxima and error words
@@ -1161,7 +1263,10 @@ template <int WPB, bool SMOOTH, int BED, bool EXACT, bool MANNING, bool EARLY>
 constexpr size_t step_smem_bytes() {
     constexpr int D = step_stages<EXACT, BED == 0, MANNING, EARLY>();
     constexpr int NF = BED == 0 ? 3 : BED == 2 ? 4 : 5;
-    return static_cast<size_t>(WPB) * D * NF * swe_row_group(EXACT, EARLY) * 32 * 8 + WPB * D * 8;
+    constexpr size_t ring_bars = static_cast<size_t>(WPB) * D * NF * swe_row_group(EXACT, EARLY) * 32 * 8 + WPB * D * 8;
+    if constexpr (!step_tma_store<WPB, SMOOTH, BED, EXACT, MANNING, EARLY>()) return ring_bars;
+    // + per-warp TMA-store staging (two buffers), 128-byte aligned
+    return (ring_bars + 127) / 128 * 128 + static_cast<size_t>(WPB) * 2 * step_stage_doubles<EXACT, EARLY, SMOOTH ? 28 : 30>() * 8;
 }
 
 }  // namespace swe_dev

@@ -71,6 +71,9 @@ struct StepParams {
     CUtensorMap tmap_state[2];
     CUtensorMap tmap_slope;
     CUtensorMap tmap_slopex;  // the dz/dx rows only (row stride 2P; box 32 x G)
+    // TMA-store epilogue: state buffer k as [3*(nloc+2R) field rows][R + nx]
+    // (columns past the domain clipped), box TW x 3G (one row group)
+    CUtensorMap tmap_out[2];
     double* buf[2];        // committed/candidate state, row-interleaved SoA
     const double* slope;   // dzdx/dzdy rows, same layout; nullptr for a flat bed
     const double* z_w;     // bed z at i=0 per local row
