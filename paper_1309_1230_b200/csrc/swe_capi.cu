@@ -7,6 +7,7 @@
 // with -fmad=false like the kernels.
 #include <algorithm>
 #include <cmath>
+#include <cstddef>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -772,6 +773,7 @@ EXPORT void swe_cuda_destroy(swe_ctx* c) {
 namespace {
 
 constexpr int kNcclSms = 2;  // SMs left free for NCCL kernels on strips
+constexpr long long kMultiMaxCells = 1 << 20;  // multi-step launches up to 1024^2 cells
 
 // Guided chunking: the first ~80 % of a launch's rows go out in `chunk`-row
 // items, the rest in quarter-size items, so the dynamic queue ends with short
@@ -905,6 +907,16 @@ int finish_load(swe_ctx* c, double t, swe_status* st) {
     ncta = std::max<long long>(ncta, (c->ntiles + 7 * SWE_STEP_WPB - 1) / (7 * SWE_STEP_WPB));
     c->ncta = static_cast<int>(ncta);
     c->prm.ncta = c->ncta;
+    // multi-step launches for small grids (latency-bound: launch gaps and a
+    // cold instruction cache per step); the cooperative grid must be resident
+    {
+        const char* env = std::getenv("SWE_MULTI");
+        const bool allow = !(env && env[0] == '0');
+        const int vm = swe_step_variant(true, c->smooth, c->flat, c->manning, false, c->xonly);
+        const int occm = allow ? swe_multi_occupancy(c->exact, c->smooth, vm) : 0;
+        c->multi_ok = allow && occm > 0 && static_cast<long long>(nloc) * c->g.nx <= kMultiMaxCells;
+        c->ncta_multi = std::max(1, std::min(c->ncta, occm * nsm));
+    }
     // dynamic work items: ~16 per worker, 16..128 rows each
     {
         const long long workers = ncta * SWE_STEP_WPB;
@@ -918,7 +930,10 @@ int finish_load(swe_ctx* c, double t, swe_status* st) {
         }
         // early exit: finer items (32 rows) so the active band is balanced
         // across workers and skipped at a finer grain
-        if (c->early && c->flat) ch = 32;
+        if (c->early && c->flat) {
+            ch = 32;
+            if (const char* e = std::getenv("SWE_EARLY_CHUNK")) ch = std::max(8, std::atoi(e));  // A/B hook
+        }
         ch = std::min<long long>(ch, nloc);
         c->prm.chunk = static_cast<int>(ch);
         c->prm.nchunks = static_cast<int>((nloc + ch - 1) / ch);
@@ -1222,6 +1237,10 @@ EXPORT int swe_cuda_advance_marked(swe_ctx* c, double t_end, double t_mark, uint
     int rc = write_ctl(c, st);
     if (rc) return rc;
     const bool use_graph = !(c->ex.flags & SWE_EXEC_NO_GRAPH) && (!c->tr || c->tr->capturable());
+    // small grids, one rank, no early exit: many steps per cooperative launch
+    // (swe_multi_kernel) instead of one launch per step
+    const int v_multi = swe_step_variant(true, c->smooth, c->flat, c->manning, false, c->xonly);
+    const bool use_multi = c->multi_ok && c->ex.nranks == 1 && !c->prm.early;
     // one batch = the chunks covering the steps still to run (64 at a time
     // when the run is bounded only by t_end / t_mark), launched back to back
     // without a host sync; launches after a halting step are device no-ops
@@ -1229,7 +1248,7 @@ EXPORT int swe_cuda_advance_marked(swe_ctx* c, double t_end, double t_mark, uint
         if (!max_steps) return std::vector<int>{64};
         return chunk_plan(max_steps - launched);
     };
-    if (use_graph) {  // build the first batch's graphs before the timed region
+    if (use_graph && !use_multi) {  // build the first batch's graphs before the timed region
         uint64_t par = h.step_index, sl = static_cast<uint64_t>(h.sel);
         for (int n : batch_of(0)) {
             swe_ctx::Graph* g;
@@ -1247,7 +1266,15 @@ EXPORT int swe_cuda_advance_marked(swe_ctx* c, double t_end, double t_mark, uint
         if (h.done) break;
         if (max_steps && launched >= max_steps) break;
         uint64_t par = h.step_index, sl = static_cast<uint64_t>(h.sel);
-        for (int n : batch_of(launched)) {
+        if (use_multi) {
+            const uint64_t left = max_steps ? max_steps - launched : 4096;
+            const int n = static_cast<int>(std::min<uint64_t>(left, 4096));
+            CUDA_TRY(cudaMemsetAsync(&c->d_ctl->mwork[0], 0,
+                                     sizeof(SweCtl) - offsetof(SweCtl, mwork), c->stream));
+            CUDA_TRY(swe_launch_multi(c->exact, c->smooth, v_multi, c->ncta_multi, c->stream, c->prm, n));
+            c->launches += 1;
+        }
+        for (int n : use_multi ? std::vector<int>{} : batch_of(launched)) {
             if (use_graph) {
                 swe_ctx::Graph* g;
                 rc = get_graph(c, n, static_cast<int>(par % 2), static_cast<int>(sl % 2), &g, st);

@@ -35,6 +35,25 @@ cudaError_t swe_launch_schedule_exact(cudaStream_t stream, const StepParams& p);
 cudaError_t swe_launch_schedule_fast(cudaStream_t stream, const StepParams& p);
 cudaError_t swe_launch_finalize(cudaStream_t stream, const StepParams& p);
 
+// multi-step kernel (small grids, one rank, no early exit): per (smooth, mode) TU
+cudaError_t swe_multi_launch0_0(int variant, int grid, cudaStream_t s, const StepParams& p, int nsteps);
+cudaError_t swe_multi_launch0_1(int variant, int grid, cudaStream_t s, const StepParams& p, int nsteps);
+cudaError_t swe_multi_launch1_0(int variant, int grid, cudaStream_t s, const StepParams& p, int nsteps);
+cudaError_t swe_multi_launch1_1(int variant, int grid, cudaStream_t s, const StepParams& p, int nsteps);
+int swe_multi_occ0_0(int variant);
+int swe_multi_occ0_1(int variant);
+int swe_multi_occ1_0(int variant);
+int swe_multi_occ1_1(int variant);
+inline cudaError_t swe_launch_multi(bool exact, bool smooth, int variant, int grid, cudaStream_t s,
+                                    const StepParams& p, int nsteps) {
+    if (smooth) return exact ? swe_multi_launch1_1(variant, grid, s, p, nsteps) : swe_multi_launch1_0(variant, grid, s, p, nsteps);
+    return exact ? swe_multi_launch0_1(variant, grid, s, p, nsteps) : swe_multi_launch0_0(variant, grid, s, p, nsteps);
+}
+inline int swe_multi_occupancy(bool exact, bool smooth, int variant) {
+    if (smooth) return exact ? swe_multi_occ1_1(variant) : swe_multi_occ1_0(variant);
+    return exact ? swe_multi_occ0_1(variant) : swe_multi_occ0_0(variant);
+}
+
 inline cudaError_t swe_launch_step(bool exact, int variant, int grid, cudaStream_t stream, const StepParams& p) {
     return exact ? swe_launch_step_exact(variant, grid, stream, p) : swe_launch_step_fast(variant, grid, stream, p);
 }

@@ -57,6 +57,8 @@ struct swe_ctx {
     StepParams prm{};
     int ncta = 0;
     int occ = 1;
+    bool multi_ok = false;  // small grid: advance() runs many steps per launch (swe_multi_kernel)
+    int ncta_multi = 0;
     // CUDA graphs of `len` consecutive steps, keyed by (len, parity of the
     // first step, committed selector at the start -- strips only: the halo
     // send/recv addresses depend on it); built on first use

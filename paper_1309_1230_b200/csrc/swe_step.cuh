@@ -177,60 +177,75 @@ __device__ __forceinline__ int seg_list(const StepParams& p, long long w, long l
 
 // --------------------------------------------------------------- finalize
 // executor.hpp:889-903 (K5/K6 outcome) + 1091-1104 (finish_dt) + 836-840 (commit).
-__device__ __forceinline__ void finalize_step(const StepParams& p, SweCtl* c, double dt, double tc) {
-    volatile unsigned long long* red = c->red;
+struct StepOutcome {
+    int status, kind, ei, ej, dflags;
+    double et, edt, dt_next, msx, msy;
+};
+
+__device__ __forceinline__ StepOutcome finalize_compute(const StepParams& p, const volatile unsigned long long* red,
+                                                        double tc) {
     const unsigned long long e2 = red[RED_E2], e4 = red[RED_E4], e5 = red[RED_E5];
     const unsigned long long dg = red[RED_DIAG], dry = red[RED_DRY];
-    const double msx = __longlong_as_double(static_cast<long long>(red[RED_SX]));
-    const double msy = __longlong_as_double(static_cast<long long>(red[RED_SY]));
-    int status = 0, kind = 0, ei = -1, ej = -1, dflags = 0;
-    double et = 0.0, edt = 0.0, dt_next = 0.0;
+    StepOutcome o{0, 0, -1, -1, 0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    o.msx = __longlong_as_double(static_cast<long long>(red[RED_SX]));
+    o.msy = __longlong_as_double(static_cast<long long>(red[RED_SY]));
     // plan order (executor.hpp:846-911): K2 precondition, K4 dry U*, K5 guard, K6
     if (e2) {
-        status = SWE_ERR_INSTABILITY; kind = 2;
+        o.status = SWE_ERR_INSTABILITY; o.kind = 2;
     } else if (dry) {
         // an interior window saw a dry U*: the host finds the row-major first
         // consumer over the whole grid (dry_scan_kernel), then K5/K6
-        status = SWE_STATUS_DIAG;
-        dflags = 2 | (e5 ? 1 : 0);
+        o.status = SWE_STATUS_DIAG;
+        o.dflags = 2 | (e5 ? 1 : 0);
     } else if (e4) {
         const unsigned long long idx = ~e4;
-        status = SWE_ERR_INSTABILITY; kind = 4;
-        ei = static_cast<int>(idx % static_cast<unsigned long long>(p.nx));
-        ej = static_cast<int>(idx / static_cast<unsigned long long>(p.nx));
-        et = tc;
-    } else if (e5 || dg || p.always_diag || !(msx < p.tz_x) || !(msy < p.tz_y)) {
+        o.status = SWE_ERR_INSTABILITY; o.kind = 4;
+        o.ei = static_cast<int>(idx % static_cast<unsigned long long>(p.nx));
+        o.ej = static_cast<int>(idx / static_cast<unsigned long long>(p.nx));
+        o.et = tc;
+    } else if (e5 || dg || p.always_diag || !(o.msx < p.tz_x) || !(o.msy < p.tz_y)) {
         // guard screen failed (first offender and values from the exact scan)
         // or dx/sx may round to 0 / overflow: exact per-cell K5 + K6 scan
-        status = SWE_STATUS_DIAG;
-        dflags = e5 ? 1 : 0;
+        o.status = SWE_STATUS_DIAG;
+        o.dflags = e5 ? 1 : 0;
     } else {
-        const double a = __ddiv_rn(p.dx, msx);
-        const double b = __ddiv_rn(p.dy, msy);
+        const double a = __ddiv_rn(p.dx, o.msx);
+        const double b = __ddiv_rn(p.dy, o.msy);
         const double core = (b < a) ? b : a;
         const double dt_raw = std_min(p.cfl * core, p.dt_max);
-        dt_next = dt_raw;
+        o.dt_next = dt_raw;
         if (dt_raw < p.dt_min) {
-            status = SWE_ERR_STEP_COLLAPSE; kind = 6; edt = dt_raw; et = tc;
+            o.status = SWE_ERR_STEP_COLLAPSE; o.kind = 6; o.edt = dt_raw; o.et = tc;
         }
     }
-    c->diag_flags = dflags;
-    c->max_sx = msx;
-    c->max_sy = msy;
+    return o;
+}
+
+// The launch's results into the control block (the host reads them).
+__device__ __forceinline__ void write_outcome(SweCtl* c, const StepOutcome& o, double dt, double tc) {
+    c->diag_flags = o.dflags;
+    c->max_sx = o.msx;
+    c->max_sy = o.msy;
     c->dt_used = dt;
     c->t_commit = tc;
-    c->dt_next = dt_next;
-    c->status = status;
-    c->err_kind = kind;
-    c->err_i = ei;
-    c->err_j = ej;
-    c->err_t = et;
-    c->err_dt = edt;
-    if (status == 0) {
+    c->dt_next = o.dt_next;
+    c->status = o.status;
+    c->err_kind = o.kind;
+    c->err_i = o.ei;
+    c->err_j = o.ej;
+    c->err_t = o.et;
+    c->err_dt = o.edt;
+}
+
+__device__ __forceinline__ void finalize_step(const StepParams& p, SweCtl* c, double dt, double tc) {
+    volatile unsigned long long* red = c->red;
+    const StepOutcome o = finalize_compute(p, red, tc);
+    write_outcome(c, o, dt, tc);
+    if (o.status == 0) {
         c->sel ^= 1;
         c->t = tc;
         c->step_index += 1ull;
-        c->dt_raw = dt_next;
+        c->dt_raw = o.dt_next;
         c->steps_done += 1ull;
         c->done = (c->mode == 1) ? (!(tc < c->t_end) || tc >= c->t_mark) : 0;
     } else {
@@ -363,6 +378,8 @@ struct Marcher {
     // qn &= bits(h) & ~mom end equal iff every cell is (H, +0, +0), same H
     unsigned long long qo, qn;
     unsigned nitems;  // items of this launch (all, or the active list)
+    unsigned* wctr;   // the step's work-item counter (null: static assignment from sclaim)
+    unsigned sclaim;
     CellVec pend;     // SWE_CFL_DEFER: output cell whose CFL speeds are pending
     bool pvalid;
 
@@ -388,8 +405,13 @@ struct Marcher {
     // built for this step (quiet items already accounted for).
     __device__ __forceinline__ void prod_seg() {
         unsigned item = 0;
-        if (lane == 0) item = atomicAdd(&p.ctl->work[p.wslot], 1u);
-        item = __shfl_sync(FULL, item, 0);
+        if (wctr) {
+            if (lane == 0) item = atomicAdd(wctr, 1u);
+            item = __shfl_sync(FULL, item, 0);
+        } else {  // static assignment (multi-step launches): items w, w + W, ...
+            item = sclaim;
+            sclaim += gridDim.x * WPB;
+        }
         if (item >= nitems) {
             pleft = 0;
             pdone = true;
@@ -1118,6 +1140,7 @@ __global__ void __launch_bounds__(WPB * 32, (step_min_blocks<EXACT, BED == 0, MA
     m.g_ok = true;
     m.d_ok = true;
     m.nitems = EARLY ? s_nact : static_cast<unsigned>(p.ntiles) * static_cast<unsigned>(p.nchunks);  // this launch's items
+    m.wctr = &ctl->work[p.wslot];
     m.qo = 0ull;
     m.qn = ~0ull;
     m.pend = {1.0, 0.0, 0.0};
@@ -1256,6 +1279,223 @@ __global__ void __launch_bounds__(256) swe_schedule_kernel(const __grid_constant
             atomicMax(&ctl->red[RED_SY], dbits(m));
             atomicAdd(&p.stats[0], n);
         }
+    }
+}
+
+// ------------------------------------------------------------ multi-step launch
+// Small grids (C1 256^2, C2 512^2: the state sits in L2) are bound by per-launch
+// latency -- launch gaps, an instruction cache refilled for the other sweep
+// parity's kernel, TMA descriptor fetches, ring fill -- not by the step's
+// work.  swe_multi_kernel runs up to `nsteps` steps of the device-resident
+// run loop (mode 1, run.hpp:149-163) in ONE cooperative launch: both sweep
+// directions are in the kernel, every CTA keeps the committed scalars (t,
+// dt_raw, selector, step index) in shared memory and recomputes the finalize
+// from the step's reduction words after a grid barrier, so the arithmetic,
+// the landing clamp and the error outcome are those of the one-step kernel
+// (finalize_compute), bit for bit.  Work counters and reduction words are
+// triple-buffered by step (the buffer of step s+1 is cleared during step s:
+// every CTA stopped reading it before the barrier of step s-1).  A failed
+// step stops every CTA; the host resolves it as after a one-step launch.
+#ifndef SWE_MULTI_STATIC
+#define SWE_MULTI_STATIC 1  // static item assignment in multi-step launches (no per-item atomics)
+#endif
+__device__ __forceinline__ void grid_barrier(SweCtl* c, unsigned nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* gen = &c->bar_gen;
+        const unsigned g = *gen;
+        __threadfence();
+        if (atomicAdd(&c->bar_count, 1u) == nblocks - 1u) {
+            c->bar_count = 0u;
+            __threadfence();
+            atomicAdd(&c->bar_gen, 1u);
+        } else {
+            while (*gen == g) __nanosleep(32);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+template <int WPB, bool FWD, bool SMOOTH, int BED, bool MANNING, bool EXACT>
+__device__ __forceinline__ void multi_step_body(const StepParams& p, double* stage, unsigned long long* bars,
+                                                Seg* segq, double* sstage, int lane, int warp, int sel, double dt,
+                                                unsigned* wctr, unsigned long long* red, WarpRing& ring,
+                                                double (*s_red)[WPB]) {
+    using M = Marcher<WPB, FWD, SMOOTH, BED, MANNING, EXACT, false>;
+    constexpr unsigned FULL = 0xffffffffu;
+    M m{p};
+    m.stage = stage;
+    m.bars = bars;
+    m.segq = segq;
+    m.qhead = 0;
+    m.qtail = 0;
+    m.lane = lane;
+    m.cur = p.buf[sel];
+    m.sel = sel;
+    m.px = 0;
+    m.py = 0;
+    m.nxt = p.buf[sel ^ 1];
+    m.P = p.pitch;
+    m.dt = dt;
+    m.dtdx = dt / p.dx;  // scheme.hpp:110, 188-190
+    m.dtdy = dt / p.dy;
+    m.half_dt = 0.5 * dt;
+    m.cx = EXACT ? m.dtdx : 0.5 * m.dtdx;
+    m.cy = EXACT ? m.dtdy : 0.5 * m.dtdy;
+    m.pleft = 0;
+    m.pdone = false;
+    m.ring = ring;  // the ring continues across steps: slot pn % D == ring.d
+    m.pn = ring.d;
+    m.req = ring.d;
+    m.mx = 0.0;
+    m.my = 0.0;
+    m.e2 = 0;
+    m.e4 = 0ull;
+    m.g_ok = true;
+    m.d_ok = true;
+    m.nitems = static_cast<unsigned>(p.ntiles) * static_cast<unsigned>(p.nchunks);
+    m.wctr = SWE_MULTI_STATIC ? nullptr : wctr;
+    m.sclaim = blockIdx.x * WPB + warp;
+    m.qo = 0ull;
+    m.qn = ~0ull;
+    m.pend = {1.0, 0.0, 0.0};
+    m.pvalid = false;
+    m.sstage = sstage;
+    m.sgrp = 0u;
+    m.produce();
+    while (m.qhead < m.qtail) {
+        const Seg sg = m.segq[m.qhead % M::QN];
+        ++m.qhead;
+        m.segment(sg);
+    }
+    if constexpr (M::TSTORE) {
+        if (lane == 0) bulk_wait_all();
+        __syncwarp();
+    }
+    ring = m.ring;
+    double mx = m.mx, my = m.my;
+    for (int o = 16; o > 0; o >>= 1) {
+        mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
+        my = fmax(my, __shfl_xor_sync(FULL, my, o));
+    }
+    if (lane == 0) {
+        s_red[0][warp] = mx;
+        s_red[1][warp] = my;
+    }
+    if (m.e2) atomicMax(&red[RED_E2], 1ull);
+    if (m.e4) atomicMax(&red[RED_E4], m.e4);
+    if (!m.g_ok) atomicMax(&red[RED_E5], 1ull);
+    if (!m.d_ok) atomicMax(&red[RED_DRY], 1ull);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = s_red[0][0], b = s_red[1][0];
+        for (int w = 1; w < WPB; ++w) {
+            a = fmax(a, s_red[0][w]);
+            b = fmax(b, s_red[1][w]);
+        }
+        atomicMax(&red[RED_SX], dbits(a));
+        atomicMax(&red[RED_SY], dbits(b));
+    }
+}
+
+template <int WPB, bool SMOOTH, int BED, bool MANNING, bool EXACT>
+__global__ void __launch_bounds__(WPB * 32, (step_min_blocks<EXACT, BED == 0, MANNING>()))
+    swe_multi_kernel(const __grid_constant__ StepParams p, int nsteps) {
+    using MF = Marcher<WPB, true, SMOOTH, BED, MANNING, EXACT, false>;
+    constexpr int D = MF::D;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int lane = tid & 31;
+    __shared__ Seg segq_all[WPB][MF::QN];
+    __shared__ double s_red[2][WPB];
+    __shared__ double s_t, s_dtraw, s_dt, s_tc, s_te, s_tm;
+    __shared__ unsigned long long s_idx, s_steps;
+    __shared__ int s_sel, s_done, s_go;
+    SweCtl* ctl = p.ctl;
+    double* stage = reinterpret_cast<double*>(smem_raw) + warp * (D * MF::SLOT);
+    unsigned long long* bars =
+        reinterpret_cast<unsigned long long*>(reinterpret_cast<double*>(smem_raw) + WPB * D * MF::SLOT) + warp * D;
+    constexpr size_t kStageOff = (static_cast<size_t>(WPB) * D * MF::SLOT * 8 + WPB * D * 8 + 127) / 128 * 128;
+    double* sstage = reinterpret_cast<double*>(smem_raw + kStageOff) + warp * 2 * MF::SD;
+    if (tid == 0) {
+        const volatile SweCtl* vc = ctl;
+        s_t = vc->t;
+        s_dtraw = vc->dt_raw;
+        s_te = vc->t_end;
+        s_tm = vc->t_mark;
+        s_idx = vc->step_index;
+        s_steps = vc->steps_done;
+        s_sel = vc->sel;
+        s_done = vc->done;
+    }
+    if (lane == 0) {
+        for (int d = 0; d < D; ++d) mbar_init(&bars[d], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    WarpRing ring{0, 0u};
+    StepOutcome last{0, 0, -1, -1, 0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    double last_dt = 0.0, last_tc = 0.0;
+    bool ran = false;
+    for (int s = 0; s < nsteps; ++s) {
+        if (tid == 0) {
+            const double t = s_t, te = s_te, dr = s_dtraw;
+            const double remaining = te - t;  // run.hpp:150-153
+            const bool landing = dr >= remaining;
+            s_dt = landing ? remaining : dr;
+            s_tc = landing ? te : t + s_dt;
+            s_go = !s_done && (t < te);
+        }
+        __syncthreads();
+        if (!s_go) break;  // identical in every CTA: the state is
+        const int b3 = s % 3, n3 = (s + 1) % 3;
+        if (blockIdx.x == 0) {  // clear the next step's buffers (see above)
+            if (tid < RED_N) ctl->mred[n3][tid] = 0ull;
+            if (tid == 0) ctl->mwork[n3] = 0u;
+        }
+        if (s > 0 && lane == 0)  // the previous step's STG outputs are this step's TMA inputs
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+        __syncwarp();
+        if ((s_idx % 2ull) == 0ull)  // scheme.hpp:86-88
+            multi_step_body<WPB, true, SMOOTH, BED, MANNING, EXACT>(p, stage, bars, segq_all[warp], sstage, lane,
+                                                                   warp, s_sel, s_dt, &ctl->mwork[b3],
+                                                                   ctl->mred[b3], ring, s_red);
+        else
+            multi_step_body<WPB, false, SMOOTH, BED, MANNING, EXACT>(p, stage, bars, segq_all[warp], sstage, lane,
+                                                                    warp, s_sel, s_dt, &ctl->mwork[b3],
+                                                                    ctl->mred[b3], ring, s_red);
+        __threadfence();
+        grid_barrier(ctl, gridDim.x);
+        if (tid == 0) {
+            const StepOutcome o = finalize_compute(p, ctl->mred[b3], s_tc);
+            last = o;
+            last_dt = s_dt;
+            last_tc = s_tc;
+            ran = true;
+            if (o.status == 0) {
+                s_sel ^= 1;
+                s_t = s_tc;
+                s_idx += 1ull;
+                s_dtraw = o.dt_next;
+                s_steps += 1ull;
+                s_done = (!(s_tc < s_te) || s_tc >= s_tm) ? 1 : 0;
+            } else {
+                s_done = 1;
+            }
+        }
+        __syncthreads();
+    }
+    if (blockIdx.x == 0 && tid == 0) {  // the run's state for the host (every CTA holds the same)
+        if (ran) write_outcome(ctl, last, last_dt, last_tc);
+        ctl->sel = s_sel;
+        ctl->t = s_t;
+        ctl->step_index = s_idx;
+        ctl->dt_raw = s_dtraw;
+        ctl->steps_done = s_steps;
+        ctl->done = s_done;
+        __threadfence();
     }
 }
 

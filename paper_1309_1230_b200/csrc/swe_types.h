@@ -59,7 +59,13 @@ struct __align__(16) SweCtl {
     unsigned int nactive;         // early exit: length of the step's active item list
     unsigned long long red[RED_N];
     int diag_flags;               // status 7: 1 = guard screen failed, 2 = interior dry U*
-    int pad_;
+    // multi-step launches (swe_multi_kernel, small grids): per-step work
+    // counters and reduction words, triple-buffered by step, and the grid
+    // barrier's arrival counter / generation
+    unsigned int mwork[3];
+    unsigned int bar_count, bar_gen;
+    unsigned int pad_[3];
+    unsigned long long mred[3][RED_N];
 };
 
 #define SWE_STATUS_DIAG 7

@@ -271,7 +271,8 @@ def test_launch_count_is_one_kernel_per_step():
     g.load(sc.build())
     n0 = g.launch_count()
     g.advance(1e18, 0, math.nan, 128)
-    assert g.launch_count() - n0 == 128
+    # one step kernel per step, or (small grids) one multi-step launch
+    assert g.launch_count() - n0 in (128, 1)
 
 
 @pytest.mark.parametrize("edge", ["north", "south", "east", "west"])

@@ -9,6 +9,10 @@ for e in 1 0; do for k in 0 1 2 3; do
 $NV -fmad=false -DSWE_EXACT_TU=$e -DSWE_PART=$k "$@" -c paper_1309_1230_b200/csrc/swe_step_inst.cu -o $out/s${e}${k}.o &
 objs="$objs $out/s${e}${k}.o"
 done; done
+for e in 1 0; do for k in 0 1; do
+$NV -fmad=false -DSWE_EXACT_TU=$e -DSWE_SMOOTH=$k "$@" -c paper_1309_1230_b200/csrc/swe_multi_inst.cu -o $out/m${e}${k}.o &
+objs="$objs $out/m${e}${k}.o"
+done; done
 for f in swe_capi swe_aux swe_transport; do
 $NV -fmad=false "$@" -c paper_1309_1230_b200/csrc/$f.cu -o $out/$f.o &
 objs="$objs $out/$f.o"
