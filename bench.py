@@ -284,7 +284,7 @@ def timed_run(sc, kind, nccl_id, args, dist, local, sampler=None, steps=None):
     return dev_s, launches, (r1 - r0) * sc.spec.nx, skipped
 
 
-def e2e_run(sc, kind, steps, nccl_id=None, dist=None, local=0):
+def e2e_run(sc, kind, steps, nccl_id=None, dist=None, local=0, api="step"):
     """The reference-facing API end to end: host FieldSet (pinned) -> load ->
     K x Stepper.step() (dt_next read back each step) -> state() to host.
     With N ranks every rank moves its own strip; the time is the max over ranks."""
@@ -306,9 +306,12 @@ def e2e_run(sc, kind, steps, nccl_id=None, dist=None, local=0):
     t0 = time.perf_counter()
     st.load_rows(*[p.numpy() for p in pinned], t=0.0)
     t1 = time.perf_counter()
-    dt = st.compute_dt(math.inf)
-    for k in range(steps):
-        dt = st.step(dt, k).dt_next
+    if api == "advance":
+        st.advance(1e18, 0, math.nan, steps)  # run_from's loop on the device (swe_cuda_advance)
+    else:
+        dt = st.compute_dt(math.inf)
+        for k in range(steps):
+            dt = st.step(dt, k).dt_next
     t2 = time.perf_counter()
     st.state_rows(*[o.numpy() for o in outs])
     el = time.perf_counter() - t0
@@ -324,8 +327,10 @@ def e2e_run(sc, kind, steps, nccl_id=None, dist=None, local=0):
     return {"value": cells * steps / el, "unit": "cell-steps/s",
             "h2d_bytes_per_step": (4 * cells * 8) // steps + ctl, "d2h_bytes_per_step": (3 * cells * 8) // steps + ctl,
             "steps": steps, "seconds": round(el, 4), "phases": phases,
-            "api": "Stepper.load(host, pinned) + K x Stepper.step() (dt_next read back each step) + "
-                   "Stepper.state() (host); C-ABI swe_cuda_load/step/state" +
+            "api": ("Stepper.load(host, pinned) + K x Stepper.step() (dt_next read back each step) + "
+                    "Stepper.state() (host); C-ABI swe_cuda_load/step/state" if api == "step" else
+                    "Stepper.load(host, pinned) + Stepper.advance(K) (run_from's loop on the device, CUDA graphs) + "
+                    "Stepper.state() (host); C-ABI swe_cuda_load/advance/state") +
                    ("; every rank moves its own strip, max over ranks" if kind.nranks > 1 else "")}
 
 
@@ -501,6 +506,8 @@ def main():
     if spec.cell_count() // world <= 16384 * 16384:
         ke = ExecutorKind(exact=head_exact, device=local, rank=rank, nranks=world, early_exit=early)
         e2e = e2e_run(sc, ke, args.e2e_steps, new_id(), dist, local)
+        # the same through the device-resident loop (no per-step host round trip)
+        e2e["advance_api"] = e2e_run(sc, ke, args.e2e_steps, new_id(), dist, local, api="advance")
 
     strong = None
     if world > 1:

@@ -17,8 +17,11 @@
 #ifndef SWE_EXACT_ROW_GROUP
 #define SWE_EXACT_ROW_GROUP 2
 #endif
+#ifndef SWE_EARLY_ROW_GROUP
+#define SWE_EARLY_ROW_GROUP 2
+#endif
 constexpr int swe_row_group(bool exact, bool early = false) {
-    return early ? 2 : exact ? SWE_EXACT_ROW_GROUP : 4;
+    return early ? (exact ? 2 : SWE_EARLY_ROW_GROUP) : exact ? SWE_EXACT_ROW_GROUP : 4;
 }
 
 // bit 16: early-exit instantiation (flat bed only); bit 32: sloped bed whose
