@@ -11,7 +11,7 @@ constexpr int swe_dev_edge_n = SWE_EDGE_N, swe_dev_edge_s = SWE_EDGE_S, swe_dev_
               swe_dev_edge_w = SWE_EDGE_W;
 
 __device__ __forceinline__ size_t pidx(int P, int R, int lr, int f, int i) {
-    return (static_cast<size_t>(lr + R) * 3 + f) * P + static_cast<size_t>(i + R);
+    return (static_cast<size_t>(lr + R) * 3 + f) * P + static_cast<size_t>(i + SWE_XO);
 }
 
 // Fill the whole padded buffer (every field row, all columns) with a benign
@@ -85,8 +85,8 @@ __global__ void slopes_kernel(const double* zp, double* slope, int P, int R, int
         const bool own = j >= 0 && j < ny;
         const double* zr = zp + static_cast<size_t>(lr + R + 1) * nx;  // bed row j
         const int js = max(j - 1, 0) - j, jn = min(j + 1, ny - 1) - j;    // clamped row offsets
-        double* sxr = slope + (static_cast<size_t>(rr) * 2 + 0) * P + R;
-        double* syr = slope + (static_cast<size_t>(rr) * 2 + 1) * P + R;
+        double* sxr = slope + (static_cast<size_t>(rr) * 2 + 0) * P + SWE_XO;
+        double* syr = slope + (static_cast<size_t>(rr) * 2 + 1) * P + SWE_XO;
         for (int i = threadIdx.x; i < nx; i += blockDim.x) {
             double sx = 0.0, sy = 0.0;
             if (own) {  // make_domain_ctx (executor.hpp:351-376): clamped central differences
@@ -131,7 +131,7 @@ __global__ void item_flat_kernel(const double* slope, int P, int R, int nx, int 
         int bad = 0;
         for (int k = threadIdx.x; k < (y1 - y0) * w; k += blockDim.x) {
             const int lr = y0 + k / w, i = x0 + k % w;
-            const size_t o = (static_cast<size_t>(lr + R) * 2) * P + (i + R);
+            const size_t o = (static_cast<size_t>(lr + R) * 2) * P + (i + SWE_XO);
             bad |= (swe_dev::dbits(slope[o]) | swe_dev::dbits(slope[o + P])) != 0ull;
         }
         bad = __syncthreads_or(bad);

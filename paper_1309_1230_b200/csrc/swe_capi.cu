@@ -364,7 +364,7 @@ void cell_values(swe_ctx* c, int which, unsigned long long idx, double* h, doubl
     if (lr < 0 || lr >= c->nloc) return;
     double v[3];
     for (int f = 0; f < 3; ++f)
-        cudaMemcpy(&v[f], c->d_buf[which] + (static_cast<size_t>(lr + c->R) * 3 + f) * c->pitch + (i + c->R), 8,
+        cudaMemcpy(&v[f], c->d_buf[which] + (static_cast<size_t>(lr + c->R) * 3 + f) * c->pitch + (i + SWE_XO), 8,
                    cudaMemcpyDeviceToHost);
     *h = v[0];
     *qx = v[1];
@@ -386,7 +386,7 @@ double dry_star_depth(swe_ctx* c, int i, int j, double dt, bool fwd) {
     double v[3][3][3];  // [row][field][col]
     for (int r = 0; r < 3; ++r)
         for (int f = 0; f < 3; ++f)
-            cudaMemcpy(v[r][f], c->d_buf[c->sel] + (static_cast<size_t>(lj - 1 + r + R) * 3 + f) * P + (i - 1 + R),
+            cudaMemcpy(v[r][f], c->d_buf[c->sel] + (static_cast<size_t>(lj - 1 + r + R) * 3 + f) * P + (i - 1 + SWE_XO),
                        3 * sizeof(double), cudaMemcpyDeviceToHost);
     const double dtdx = dt / c->g.dx, dtdy = dt / c->g.dy;
     const int s = fwd ? 1 : -1;
@@ -631,7 +631,8 @@ EXPORT int swe_cuda_create(const swe_grid* grid, const swe_physics* phys, const 
     c->nloc = bands[ex.rank].second - bands[ex.rank].first;
     const int out_w = SWE_TILE_W(c->R);
     c->ntiles = (grid->nx + out_w - 1) / out_w;
-    c->pitch = ((c->ntiles * out_w + 2 * c->R + 32) + 31) / 32 * 32;
+    // columns touched: the last window's load box ends at ntiles*TW - R + SWE_XO + 33
+    c->pitch = ((c->ntiles * out_w + SWE_XO + 34) + 31) / 32 * 32;
     const size_t rows = static_cast<size_t>(c->nloc + 2 * c->R);
     c->buf_doubles = rows * 3 * c->pitch;
     *out = c;
@@ -692,7 +693,8 @@ EXPORT int swe_cuda_create(const swe_grid* grid, const swe_physics* phys, const 
     {
         std::string err;
         for (int k = 0; k < 2; ++k)
-            if (!encode_rows(&p.tmap_state[k], c->d_buf[k], c->pitch, static_cast<long long>(rows) * 3, 3 * swe_row_group(c->exact), err))
+            if (!encode_rows(&p.tmap_state[k], c->d_buf[k], c->pitch, static_cast<long long>(rows) * 3,
+                             3 * swe_row_group(c->exact), err, swe_box_w(c->R)))
                 return set_status(st, SWE_ERR_RUNTIME, -1, -1, 0, "%s", err.c_str());
     }
     p.buf[0] = c->d_buf[0];
@@ -853,19 +855,21 @@ int finish_load(swe_ctx* c, double t, swe_status* st) {
         const int G = swe_row_group(c->exact, c->early && c->flat);
         for (int k = 0; k < 2; ++k)
             if (!encode_rows(&c->prm.tmap_state[k], c->d_buf[k], P, static_cast<long long>(nloc + 2 * R) * 3, 3 * G,
-                             err))
+                             err, swe_box_w(R)))
                 return set_status(st, SWE_ERR_RUNTIME, -1, -1, 0, "%s", err.c_str());
-        if (!encode_rows(&c->prm.tmap_slope, c->d_slope, P, static_cast<long long>(nloc + 2 * R) * 2, 2 * G, err))
+        if (!encode_rows(&c->prm.tmap_slope, c->d_slope, P, static_cast<long long>(nloc + 2 * R) * 2, 2 * G, err,
+                         swe_box_w(R)))
             return set_status(st, SWE_ERR_RUNTIME, -1, -1, 0, "%s", err.c_str());
-        // TMA-store epilogue: inner extent R + nx (the window's out-of-domain
-        // columns are clipped), rows 3*(nloc+2R), pitch P
+        // TMA-store epilogue: inner extent SWE_XO + nx (the window's
+        // out-of-domain columns are clipped), rows 3*(nloc+2R), pitch P
         const int TW = SWE_TILE_W(R);
         for (int k = 0; k < 2; ++k) {
-            if (!encode_rows(&c->prm.tmap_out[k], c->d_buf[k], R + nx, static_cast<long long>(nloc + 2 * R) * 3, 3 * G,
-                             err, TW, P))
+            if (!encode_rows(&c->prm.tmap_out[k], c->d_buf[k], SWE_XO + nx, static_cast<long long>(nloc + 2 * R) * 3,
+                             3 * G, err, TW, P))
                 return set_status(st, SWE_ERR_RUNTIME, -1, -1, 0, "%s", err.c_str());
         }
-        if (!encode_rows(&c->prm.tmap_slopex, c->d_slope, P, static_cast<long long>(nloc + 2 * R), G, err, 32, 2 * P))
+        if (!encode_rows(&c->prm.tmap_slopex, c->d_slope, P, static_cast<long long>(nloc + 2 * R), G, err,
+                         swe_box_w(R), 2 * P))
             return set_status(st, SWE_ERR_RUNTIME, -1, -1, 0, "%s", err.c_str());
     }
 
@@ -1030,7 +1034,7 @@ EXPORT int swe_cuda_load(swe_ctx* c, const double* z, const double* h, const dou
     // committed state into buffer 0 (padded, row-interleaved), bed into d_zp
     const double* src[3] = {h, qx, qy};
     for (int f = 0; f < 3; ++f) {
-        double* dst = c->d_buf[0] + (static_cast<size_t>(R) * 3 + f) * P + R;
+        double* dst = c->d_buf[0] + (static_cast<size_t>(R) * 3 + f) * P + SWE_XO;
         CUDA_TRY(cudaMemcpy2DAsync(dst, 3 * P * sizeof(double), src[f], rowb, rowb, nloc,
                                    cudaMemcpyHostToDevice, c->stream));
     }
@@ -1081,7 +1085,7 @@ EXPORT int swe_cuda_state(swe_ctx* c, double* z, double* h, double* qx, double* 
     double* dst[3] = {h, qx, qy};
     for (int f = 0; f < 3; ++f) {
         if (!dst[f]) continue;
-        const double* src = c->d_buf[c->sel] + (static_cast<size_t>(R) * 3 + f) * P + R;
+        const double* src = c->d_buf[c->sel] + (static_cast<size_t>(R) * 3 + f) * P + SWE_XO;
         CUDA_TRY(cudaMemcpy2DAsync(dst[f], rowb, src, 3 * P * sizeof(double), rowb, c->nloc,
                                    cudaMemcpyDeviceToHost, c->stream));
     }

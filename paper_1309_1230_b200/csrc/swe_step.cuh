@@ -59,6 +59,13 @@ constexpr int step_stages() {
 #endif
 }
 
+// Ring slot of one row group: the state box ([3G][BW] doubles) and the slope
+// box ([(NF-3)G][BW]), each padded to 128 bytes (TMA destination alignment).
+constexpr int swe_pad16(int n) { return (n + 15) / 16 * 16; }
+constexpr int step_slot_doubles(int NF, int G, int R) {
+    return swe_pad16(3 * G * swe_box_w(R)) + swe_pad16((NF - 3) * G * swe_box_w(R));
+}
+
 // Output staging for a TMA-store epilogue: per warp two buffers of one row
 // group ([3G field rows][TW doubles], padded to 128 B), for the variants whose
 // ring + staging fit the SM's 228 KB at their occupancy.  OFF: a TMA tensor
@@ -74,16 +81,25 @@ template <bool EXACT, bool EARLY, int TW>
 constexpr int step_stage_doubles() {
     return ((3 * swe_row_group(EXACT, EARLY) * TW * 8 + 127) / 128) * 128 / 8;
 }
+// staging buffers per warp for the TMA-store epilogue: 2 (the next group is
+// staged while the previous store reads), 1 if two do not fit, 0 = STG epilogue
 template <int WPB, bool SMOOTH, int BED, bool EXACT, bool MANNING, bool EARLY>
-constexpr bool step_tma_store() {
+constexpr int step_tma_buffers() {
     constexpr int NF = BED == 0 ? 3 : BED == 2 ? 4 : 5;
     constexpr int G = swe_row_group(EXACT, EARLY);
     constexpr int D = step_stages<EXACT, BED == 0, MANNING, EARLY>();
     constexpr int TW = SMOOTH ? 28 : 30;
-    constexpr long ring = static_cast<long>(D) * NF * G * 32 * 8;
-    constexpr long stage = 2L * step_stage_doubles<EXACT, EARLY, TW>() * 8;
-    constexpr long per_cta = WPB * (ring + stage + D * 8) + 1536;  // + static smem and the per-CTA reserve
-    return SWE_TMA_STORE != 0 && per_cta * step_min_blocks<EXACT, BED == 0, MANNING>() <= 228L * 1024;
+    constexpr long ring = static_cast<long>(D) * step_slot_doubles(NF, G, SMOOTH ? 2 : 1) * 8;
+    constexpr long stage = static_cast<long>(step_stage_doubles<EXACT, EARLY, TW>()) * 8;
+    constexpr int blocks = step_min_blocks<EXACT, BED == 0, MANNING>();
+    // + static smem and the per-CTA reserve
+    constexpr long cta2 = WPB * (ring + 2 * stage + D * 8) + 1536, cta1 = WPB * (ring + stage + D * 8) + 1536;
+    if (SWE_TMA_STORE == 0) return 0;
+    return cta2 * blocks <= 228L * 1024 ? 2 : cta1 * blocks <= 228L * 1024 ? 1 : 0;
+}
+template <int WPB, bool SMOOTH, int BED, bool EXACT, bool MANNING, bool EARLY>
+constexpr bool step_tma_store() {
+    return step_tma_buffers<WPB, SMOOTH, BED, EXACT, MANNING, EARLY>() > 0;
 }
 
 // ---------------------------------------------------------------- PTX helpers
@@ -330,10 +346,15 @@ struct Marcher {
     static constexpr int NF = FLAT ? 3 : XONLY ? 4 : 5;  // doubles per cell in the ring
     static constexpr int D = step_stages<EXACT, FLAT, MANNING, EARLY>();
     static constexpr int G = swe_row_group(EXACT, EARLY);
-    static constexpr int SLOT = NF * G * 32;  // doubles per ring slot: [G][3][32] state, [G][2][32] slopes
+    static constexpr int BW = swe_box_w(R);   // load box width (32, or 34 for R = 1: see swe_types.h)
+    static constexpr int BO = swe_box_off(R); // lane 0's column in the box
+    static constexpr int ST_D = swe_pad16(3 * G * BW);         // state box doubles in a slot (padded)
+    static constexpr int SLOT = step_slot_doubles(NF, G, R);     // doubles per ring slot: state, then slopes
+    static constexpr unsigned TX_BYTES = NF * G * BW * 8;        // bytes the slot's TMA loads deliver
     static constexpr int TW = 32 - 2 * R;
     static constexpr unsigned FULL = 0xffffffffu;
-    static constexpr bool TSTORE = step_tma_store<WPB, SMOOTH, BED, EXACT, MANNING, EARLY>();
+    static constexpr int NB = step_tma_buffers<WPB, SMOOTH, BED, EXACT, MANNING, EARLY>();  // staging buffers
+    static constexpr bool TSTORE = NB > 0;
     static constexpr int SD = step_stage_doubles<EXACT, EARLY, TW>();  // doubles per staging buffer
 
     const StepParams& p;
@@ -438,7 +459,7 @@ struct Marcher {
         ++qtail;
         pleft = ((sg.rb - sg.ra) + 2 * R + G - 1) / G;
         const int row = FWD ? sg.ra - R : sg.rb - 1 + R;  // first row in march order
-        px = sg.tile * TW;                                // padded column of x0-R
+        px = sg.tile * TW - R + SWE_XO - BO;              // load box start (lane 0's column - BO, even)
         py = (FWD ? row : row - (G - 1)) + R;             // lowest padded row of the first group
     }
     __device__ __forceinline__ void produce() {
@@ -448,12 +469,12 @@ struct Marcher {
             const int d = pn % D;
             // the box may run past the buffer at a strip end (TMA fills zeros there,
             // never consumed), but it must overlap it
-            SWE_DCHECK(px >= 0 && px + 32 <= P && py + G > 0 && py < p.nloc + 2 * R);
+            SWE_DCHECK(px >= 0 && (px & 1) == 0 && px + BW <= P && py + G > 0 && py < p.nloc + 2 * R);
             if (lane == 0) {
-                mbar_expect_tx(&bars[d], SLOT * 8);
+                mbar_expect_tx(&bars[d], TX_BYTES);
                 tma_load_2d(stage + d * SLOT, &p.tmap_state[sel], px, py * 3, &bars[d]);
-                if constexpr (XONLY) tma_load_2d(stage + d * SLOT + 3 * G * 32, &p.tmap_slopex, px, py, &bars[d]);
-                else if constexpr (!FLAT) tma_load_2d(stage + d * SLOT + 3 * G * 32, &p.tmap_slope, px, py * 2, &bars[d]);
+                if constexpr (XONLY) tma_load_2d(stage + d * SLOT + ST_D, &p.tmap_slopex, px, py, &bars[d]);
+                else if constexpr (!FLAT) tma_load_2d(stage + d * SLOT + ST_D, &p.tmap_slope, px, py * 2, &bars[d]);
             }
             py += S * G;
             --pleft;
@@ -468,15 +489,15 @@ struct Marcher {
         if constexpr (GI == 0) mbar_wait(&bars[ring.d], ring.ph);
         constexpr int g = FWD ? GI : G - 1 - GI;  // row within the box (boxes ascend in y)
         const double* st = stage + ring.d * SLOT;
-        u.h = st[g * 96 + lane];
-        u.qx = st[g * 96 + 32 + lane];
-        u.qy = st[g * 96 + 64 + lane];
+        u.h = st[g * 3 * BW + lane + BO];
+        u.qx = st[g * 3 * BW + BW + lane + BO];
+        u.qy = st[g * 3 * BW + 2 * BW + lane + BO];
         if constexpr (XONLY) {
-            zx = st[G * 96 + g * 32 + lane];
+            zx = st[ST_D + g * BW + lane + BO];
             zy = 0.0;  // the bed's dz/dy bit patterns are all +0.0
         } else if constexpr (!FLAT) {
-            zx = st[G * 96 + g * 64 + lane];
-            zy = st[G * 96 + g * 64 + 32 + lane];
+            zx = st[ST_D + g * 2 * BW + lane + BO];
+            zy = st[ST_D + g * 2 * BW + BW + lane + BO];
         } else {
             zx = 0.0;
             zy = 0.0;
@@ -544,16 +565,16 @@ struct Marcher {
         }
         if constexpr (TSTORE && SLOT >= 0) {  // stage the row for the warp's TMA store of its group
             constexpr int gr = FWD ? SLOT : G - 1 - SLOT;  // row within the box (boxes ascend in y)
-            double* sb = sstage + (sgrp & 1u) * SD + gr * 3 * TW + (lane - R);
+            double* sb = sstage + (NB == 2 ? (sgrp & 1u) * SD : 0) + gr * 3 * TW + (lane - R);
             if (on && !(SWE_ABL & 1)) {
                 sb[0] = o.h;
                 sb[TW] = o.qx;
                 sb[2 * TW] = o.qy;
             }
         }
-        double* row = orow;  // == nxt + (rr + R) * 3P + (i + R)
+        double* row = orow;  // == nxt + (rr + R) * 3P + (i + SWE_XO)
         orow += S * 3 * P;
-        SWE_DCHECK(!on || (row == nxt + (static_cast<long long>(rr + R) * 3 * P + (i + R)) && rr >= 0 && rr < p.nloc &&
+        SWE_DCHECK(!on || (row == nxt + (static_cast<long long>(rr + R) * 3 * P + (i + SWE_XO)) && rr >= 0 && rr < p.nloc &&
                            i >= 0 && i < p.nx));
         if (!(TSTORE && SLOT >= 0) && on && !(SWE_ABL & 1)) {
             row[0] = o.h;
@@ -599,7 +620,10 @@ struct Marcher {
     // (G rows x h/qx/qy x TW columns; the tensor map ends at column R + nx, so
     // the last window's out-of-domain lanes are clipped).
     __device__ __forceinline__ void group_begin() {
-        if (lane == 0) bulk_wait_read<1>();
+        if (lane == 0) {
+            if constexpr (NB == 2) bulk_wait_read<1>();
+            else bulk_wait_read<0>();
+        }
         __syncwarp();
     }
     __device__ __forceinline__ void group_flush() {
@@ -608,7 +632,8 @@ struct Marcher {
         if (lane == 0) {
             const int y0 = FWD ? erow0 + egrp * G : erow0 - (egrp + 1) * G;  // lowest row of the group
             SWE_DCHECK(y0 >= 0 && y0 + G <= p.nloc);
-            tma_store_2d(&p.tmap_out[sel ^ 1], seg_tile * TW + R, (y0 + R) * 3, sstage + (sgrp & 1u) * SD);
+            tma_store_2d(&p.tmap_out[sel ^ 1], seg_tile * TW + SWE_XO, (y0 + R) * 3,
+                         sstage + (NB == 2 ? (sgrp & 1u) * SD : 0));
             bulk_commit();
         }
         ++sgrp;
@@ -974,7 +999,7 @@ struct Marcher {
         erow0 = FWD ? sg.ra : sg.rb;
         egrp = 0;
 
-        orow = nxt + static_cast<size_t>(r_start + R) * 3 * P + (i + R);  // first output row
+        orow = nxt + static_cast<size_t>(r_start + R) * 3 * P + (i + SWE_XO);  // first output row
         qo = 0ull;
         qn = ~0ull;
         const int jlo = p.j0 + sg.ra - R - 1, jhi = p.j0 + sg.rb + R;  // rows the march touches, padded
@@ -1077,7 +1102,7 @@ __global__ void __launch_bounds__(WPB * 32, (step_min_blocks<EXACT, BED == 0, MA
         reinterpret_cast<unsigned long long*>(reinterpret_cast<double*>(smem_raw) + WPB * D * M::SLOT) + warp * D;
     // TMA-store staging: after the rings and barriers, 128-byte aligned
     constexpr size_t kStageOff = (static_cast<size_t>(WPB) * D * M::SLOT * 8 + WPB * D * 8 + 127) / 128 * 128;
-    double* sstage = reinterpret_cast<double*>(smem_raw + kStageOff) + warp * 2 * M::SD;
+    double* sstage = reinterpret_cast<double*>(smem_raw + kStageOff) + warp * M::NB * M::SD;
 
     if (tid == 0) {
         const volatile SweCtl* vc = ctl;
@@ -1418,7 +1443,7 @@ __global__ void __launch_bounds__(WPB * 32, (step_min_blocks<EXACT, BED == 0, MA
     unsigned long long* bars =
         reinterpret_cast<unsigned long long*>(reinterpret_cast<double*>(smem_raw) + WPB * D * MF::SLOT) + warp * D;
     constexpr size_t kStageOff = (static_cast<size_t>(WPB) * D * MF::SLOT * 8 + WPB * D * 8 + 127) / 128 * 128;
-    double* sstage = reinterpret_cast<double*>(smem_raw + kStageOff) + warp * 2 * MF::SD;
+    double* sstage = reinterpret_cast<double*>(smem_raw + kStageOff) + warp * MF::NB * MF::SD;
     if (tid == 0) {
         const volatile SweCtl* vc = ctl;
         s_t = vc->t;
@@ -1503,10 +1528,14 @@ template <int WPB, bool SMOOTH, int BED, bool EXACT, bool MANNING, bool EARLY>
 constexpr size_t step_smem_bytes() {
     constexpr int D = step_stages<EXACT, BED == 0, MANNING, EARLY>();
     constexpr int NF = BED == 0 ? 3 : BED == 2 ? 4 : 5;
-    constexpr size_t ring_bars = static_cast<size_t>(WPB) * D * NF * swe_row_group(EXACT, EARLY) * 32 * 8 + WPB * D * 8;
+    constexpr size_t ring_bars =
+        static_cast<size_t>(WPB) * D * step_slot_doubles(NF, swe_row_group(EXACT, EARLY), SMOOTH ? 2 : 1) * 8 +
+        WPB * D * 8;
     if constexpr (!step_tma_store<WPB, SMOOTH, BED, EXACT, MANNING, EARLY>()) return ring_bars;
-    // + per-warp TMA-store staging (two buffers), 128-byte aligned
-    return (ring_bars + 127) / 128 * 128 + static_cast<size_t>(WPB) * 2 * step_stage_doubles<EXACT, EARLY, SMOOTH ? 28 : 30>() * 8;
+    // + per-warp TMA-store staging (one or two buffers), 128-byte aligned
+    return (ring_bars + 127) / 128 * 128 + static_cast<size_t>(WPB) *
+                                               step_tma_buffers<WPB, SMOOTH, BED, EXACT, MANNING, EARLY>() *
+                                               step_stage_doubles<EXACT, EARLY, SMOOTH ? 28 : 30>() * 8;
 }
 
 }  // namespace swe_dev

@@ -10,6 +10,18 @@
 
 enum { SWE_EDGE_N = 0, SWE_EDGE_S = 1, SWE_EDGE_E = 2, SWE_EDGE_W = 3 };
 
+// Padded rows: cell i of a row sits at column i + SWE_XO.  SWE_XO is even (and
+// >= R = 1, 2) so that every window's first output column, tile * TW + SWE_XO,
+// is 16-byte aligned: TMA tensor stores must start on a 16-byte-aligned inner
+// coordinate (tools/tma_store_probe.cu).
+#define SWE_XO 2
+// TMA load box of a window (32 lanes, lane 0 at column tile*TW - R + SWE_XO):
+// with R = 1 lane 0 sits at an odd column, so the box starts one column
+// earlier and is 34 wide (16-byte-aligned start, 272-byte rows); with R = 2 it
+// starts at lane 0 and is 32 wide.
+constexpr int swe_box_off(int R) { return (SWE_XO - R) & 1; }
+constexpr int swe_box_w(int R) { return 32 + 2 * swe_box_off(R); }
+
 struct SweBC {
     int type;  // swe_bc_type
     double q_n;
