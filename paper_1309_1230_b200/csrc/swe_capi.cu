@@ -254,6 +254,28 @@ int halo_exchange(swe_ctx* c, int which, cudaStream_t s, swe_status* st) {
 // exchange only).
 int enqueue_step(swe_ctx* c, bool fwd, int cand, swe_status* st) {
     const int v = swe_step_variant(fwd, c->smooth, c->flat, c->manning, c->early, c->xonly);
+    if (c->p2p) {
+        // Strips with the fused halo push: the step kernel stores its edge rows
+        // into the neighbours' halos itself; one allreduce of the reduction
+        // words (which also orders those stores before every rank's next
+        // step), then the finalize.
+        if (c->prm.early) {
+            CUDA_TRY(swe_launch_schedule(c->exact, c->stream, c->prm));
+            ++c->launches;
+        }
+        CUDA_TRY(swe_launch_step(c->exact, v, c->ncta, c->stream, c->prm));
+        if (c->time_exchange) CUDA_TRY(cudaEventRecord(c->ev_x[2], c->stream));
+        int rc = c->tr->allreduce_max(c, c->stream, c->d_ctl->red, RED_N, st);
+        if (rc) return rc;
+        if (c->time_exchange) {
+            CUDA_TRY(cudaEventRecord(c->ev_x[3], c->stream));
+            CUDA_TRY(cudaEventRecord(c->ev_x[0], c->stream));  // no separate exchange (not counted)
+            CUDA_TRY(cudaEventRecord(c->ev_x[1], c->stream));
+        }
+        CUDA_TRY(swe_launch_finalize(c->stream, c->prm));
+        c->launches += 2 + (c->tr->capturable() ? 0 : 1);  // step + finalize (+ local max kernel)
+        return SWE_OK;
+    }
     if (c->overlap) {
         // Strips, overlapped: the edge launch (the bands whose rows the
         // neighbours need) runs on a high-priority stream and its halo
@@ -678,6 +700,31 @@ EXPORT int swe_cuda_create(const swe_grid* grid, const swe_physics* phys, const 
         CUDA_TRY(dev_alloc(reinterpret_cast<void**>(&c->d_xr), 16 * sizeof(unsigned long long)));
         const int trc = create_transport(c, ex, exec->nccl_id, st);
         if (trc) return trc;
+        // fused halo push: map the strip neighbours' buffers; used only if every
+        // rank could (an allreduce agrees), else the halo goes by send/recv
+        const char* pe = std::getenv("SWE_P2P");
+        double *dn[2] = {nullptr, nullptr}, *up[2] = {nullptr, nullptr};
+        int nloc_dn = 0;
+        if (!(pe && pe[0] == '0')) {
+            int rc2 = c->tr->peer_buffers(c, dn, up, &nloc_dn, st);
+            if (rc2) return rc2;
+        }
+        const bool mine_ok = (ex.rank == 0 || dn[0]) && (ex.rank + 1 == ex.nranks || up[0]);
+        unsigned long long bad = mine_ok ? 0ull : 1ull;
+        CUDA_TRY(cudaMemcpyAsync(c->d_scan, &bad, sizeof bad, cudaMemcpyHostToDevice, c->stream));
+        int rc3 = c->tr->allreduce_max(c, c->stream, c->d_scan, 1, st);
+        if (rc3) return rc3;
+        CUDA_TRY(cudaMemcpyAsync(&bad, c->d_scan, sizeof bad, cudaMemcpyDeviceToHost, c->stream));
+        CUDA_TRY(cudaStreamSynchronize(c->stream));
+        c->p2p = bad == 0ull;
+        if (c->p2p) {
+            for (int k = 0; k < 2; ++k) {
+                c->prm.peer_dn[k] = dn[k];
+                c->prm.peer_up[k] = up[k];
+            }
+            c->prm.nloc_dn = nloc_dn;
+            c->prm.p2p = 1;
+        }
     }
 
     // K6 diagnosis thresholds (see swe_step.cuh finalize_step)
@@ -901,7 +948,8 @@ int finish_load(swe_ctx* c, double t, swe_status* st) {
     // NCCL strips: leave two SMs to NCCL's send/recv and allreduce kernels so
     // the halo exchange runs beside the persistent interior launch instead of
     // after it (its CTAs never retire early)
-    if (c->ex.nranks > 1 && !(c->ex.flags & SWE_EXEC_LOCAL_GROUP)) nsm = std::max(1, nsm - kNcclSms);
+    // (not with the fused halo push: no send/recv runs beside the step)
+    if (c->ex.nranks > 1 && !c->p2p && !(c->ex.flags & SWE_EXEC_LOCAL_GROUP)) nsm = std::max(1, nsm - kNcclSms);
     // persistent grid: every resident warp is a worker; small grids keep at
     // least 4 rows per worker so the 2R warm-up rows stay amortised
     const long long units = static_cast<long long>(c->ntiles) * nloc;
@@ -992,7 +1040,7 @@ int finish_load(swe_ctx* c, double t, swe_status* st) {
     // launch covers the kEdge rows at each end of the strip (>= R, the rows the
     // neighbours receive); the interior launch the rows in between.
     constexpr int kEdge = 8;
-    c->overlap = c->ex.nranks > 1 && !(c->early && c->flat) && nloc >= 2 * kEdge + 16;
+    c->overlap = c->ex.nranks > 1 && !c->p2p && !(c->early && c->flat) && nloc >= 2 * kEdge + 16;
     if (c->overlap) {
         c->prm_edge = c->prm;
         c->prm_edge.chunk = kEdge;
@@ -1135,7 +1183,7 @@ EXPORT int swe_cuda_step(swe_ctx* c, double dt, uint64_t step_index, double t_af
         cudaEventElapsedTime(&mx, c->ev_x[0], c->ev_x[1]);
         cudaEventElapsedTime(&ma, c->ev_x[2], c->ev_x[3]);
         c->timing.exchange_steps += 1;
-        c->timing.exchange_seconds += mx * 1e-3;
+        if (!c->p2p) c->timing.exchange_seconds += mx * 1e-3;  // fused push: no separate exchange
         c->timing.allreduce_seconds += ma * 1e-3;
     }
     rc = resolve(c, st);

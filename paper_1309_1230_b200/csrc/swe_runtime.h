@@ -71,6 +71,7 @@ struct swe_ctx {
     unsigned long long* d_xr = nullptr;  // local-group allreduce scratch
     // strips: halo exchange overlapped with the interior (edge + interior launches)
     bool overlap = false;
+    bool p2p = false;  // strips: fused halo push into the neighbours' buffers (no send/recv per step)
     StepParams prm_edge{}, prm_int{};
     int ncta_edge = 0;
     cudaStream_t stream_edge = nullptr;
@@ -168,6 +169,11 @@ struct Transport {
     virtual int sendrecv(swe_ctx* c, cudaStream_t s, const void* send_up, void* recv_up, const void* send_down,
                          void* recv_down, size_t bytes, swe_status* st) = 0;
     virtual bool capturable() const = 0;  // may be recorded into a CUDA graph
+    // The strip neighbours' two state buffers as device pointers this rank's
+    // kernels may store to (NVLink peer memory through CUDA IPC or in-process
+    // peer access; the same device for the local group), for the fused halo
+    // push.  Collective over the group; leaves nulls when unavailable.
+    virtual int peer_buffers(swe_ctx* c, double* dn[2], double* up[2], int* nloc_dn, swe_status* st) = 0;
 };
 
 // The transport of a context with nranks > 1: NCCL between GPUs, or the local

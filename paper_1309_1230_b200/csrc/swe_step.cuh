@@ -401,6 +401,7 @@ struct Marcher {
     unsigned nitems;  // items of this launch (all, or the active list)
     unsigned* wctr;   // the step's work-item counter (null: static assignment from sclaim)
     unsigned sclaim;
+    bool pushed;      // this lane stored halo rows into a neighbour's buffer (fused halo push)
     CellVec pend;     // SWE_CFL_DEFER: output cell whose CFL speeds are pending
     bool pvalid;
 
@@ -583,6 +584,23 @@ struct Marcher {
         }
         if constexpr (!EDGE) return;
         if (!on) return;
+        double* q = nullptr;  // the neighbour's copy of this cell (fused halo push), if any
+        if (p.p2p) {
+            // fused halo push: this strip's R edge rows -- with their x ghosts,
+            // below -- go straight into the neighbours' halo rows of the same
+            // (candidate) buffer, over NVLink peer memory; the step's allreduce
+            // orders them before the neighbours' next step (no send/recv)
+            if (rr < R && p.peer_dn[sel ^ 1])
+                q = p.peer_dn[sel ^ 1] + static_cast<size_t>(p.nloc_dn + rr + R) * 3 * P + (i + SWE_XO);
+            else if (rr >= p.nloc - R && p.peer_up[sel ^ 1])
+                q = p.peer_up[sel ^ 1] + static_cast<size_t>(rr - p.nloc + R) * 3 * P + (i + SWE_XO);
+            if (q) {
+                q[0] = o.h;
+                q[P] = o.qx;
+                q[2 * P] = o.qy;
+                pushed = true;
+            }
+        }
         if (!(xedge || jj == 0 || jj == p.ny - 1)) return;
         SWE_DCHECK(row - nxt >= 3 * P && row - nxt + 2 * P + 1 < p.buf_doubles - 3 * P && rr + R < p.nloc + 2 * R);
         if (i == 0) {
@@ -590,12 +608,22 @@ struct Marcher {
             row[-1] = g.h;
             row[P - 1] = g.qx;
             row[2 * P - 1] = g.qy;
+            if (q) {
+                q[-1] = g.h;
+                q[P - 1] = g.qx;
+                q[2 * P - 1] = g.qy;
+            }
         }
         if (i == p.nx - 1) {
             const CellVec g = edge_ghost(SWE_EDGE_E, p.bc[SWE_EDGE_E], o, p.z_e[rr + R], p.h_min);
             row[1] = g.h;
             row[P + 1] = g.qx;
             row[2 * P + 1] = g.qy;
+            if (q) {
+                q[1] = g.h;
+                q[P + 1] = g.qx;
+                q[2 * P + 1] = g.qy;
+            }
         }
         if (jj == 0) {
             const CellVec g = edge_ghost(SWE_EDGE_S, p.bc[SWE_EDGE_S], o, p.z_s[i], p.h_min);
@@ -1003,8 +1031,11 @@ struct Marcher {
         qo = 0ull;
         qn = ~0ull;
         const int jlo = p.j0 + sg.ra - R - 1, jhi = p.j0 + sg.rb + R;  // rows the march touches, padded
-        if (xedge || jlo <= 0 || jhi >= p.ny - 1) march<true>();
+        // segments with strip edge rows run the edge march too (fused halo push)
+        const bool pedge = p.p2p && (sg.ra < R || sg.rb > p.nloc - R);
+        if (xedge || jlo <= 0 || jhi >= p.ny - 1 || pedge) march<true>();
         else march<false>();
+        if (pedge && __any_sync(FULL, pushed)) __threadfence_system();  // the peer stores, system-wide
         if constexpr (!EXACT && SWE_CFL_DEFER) {  // the segment's last pending cell
             double sx, sy;
             cfl_speeds_fast(pend.h, pend.qx, pend.qy, p.sqrt_g, sx, sy);
@@ -1170,6 +1201,7 @@ __global__ void __launch_bounds__(WPB * 32, (step_min_blocks<EXACT, BED == 0, MA
     m.qn = ~0ull;
     m.pend = {1.0, 0.0, 0.0};
     m.pvalid = false;
+    m.pushed = false;
     m.sstage = sstage;
     m.sgrp = 0u;
     m.produce();
@@ -1386,6 +1418,7 @@ __device__ __forceinline__ void multi_step_body(const StepParams& p, double* sta
     m.qn = ~0ull;
     m.pend = {1.0, 0.0, 0.0};
     m.pvalid = false;
+    m.pushed = false;
     m.sstage = sstage;
     m.sgrp = 0u;
     m.produce();

@@ -1,6 +1,7 @@
 // swe_transport.cu — row-strip collectives: NCCL (dlopen'ed, between GPUs) and
 // the local group (contexts of one process on one device, for single-GPU tests).
 #include <dlfcn.h>
+#include <unistd.h>
 
 #include <chrono>
 #include <cstdio>
@@ -8,6 +9,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include <nccl.h>
 
@@ -82,7 +84,9 @@ std::map<std::string, CommEntry> g_comms;
 struct NcclTransport final : Transport {
     ncclComm_t comm = nullptr;
     std::string key;
+    std::vector<void*> ipc_opened;  // neighbour buffers mapped through CUDA IPC (closed with the transport)
     ~NcclTransport() override {
+        for (void* q : ipc_opened) cudaIpcCloseMemHandle(q);
         std::lock_guard<std::mutex> lk(g_comms_m);
         auto it = g_comms.find(key);
         if (it != g_comms.end() && --it->second.refs == 0) {
@@ -94,6 +98,7 @@ struct NcclTransport final : Transport {
     int sendrecv(swe_ctx* c, cudaStream_t s, const void* su, void* ru, const void* sd, void* rd, size_t bytes,
                  swe_status* st) override;
     bool capturable() const override { return true; }
+    int peer_buffers(swe_ctx* c, double* dn[2], double* up[2], int* nloc_dn, swe_status* st) override;
 };
 
 
@@ -107,6 +112,8 @@ struct LocalGroup {
     const void* su[kMaxLocalRanks] = {};
     const void* sd[kMaxLocalRanks] = {};
     const unsigned long long* red[kMaxLocalRanks] = {};
+    double* buf[kMaxLocalRanks][2] = {};  // every rank's state buffers (fused halo push)
+    int nloc[kMaxLocalRanks] = {};
     // all ranks arrive (or a 120 s timeout breaks the group, so a failing
     // test cannot hang the box)
     bool barrier() {
@@ -149,6 +156,7 @@ struct LocalTransport final : Transport {
     int sendrecv(swe_ctx* c, cudaStream_t s, const void* su, void* ru, const void* sd, void* rd, size_t bytes,
                  swe_status* st) override;
     bool capturable() const override { return false; }
+    int peer_buffers(swe_ctx* c, double* dn[2], double* up[2], int* nloc_dn, swe_status* st) override;
 };
 
 }  // namespace
@@ -221,7 +229,93 @@ int LocalTransport::allreduce_max(swe_ctx* c, cudaStream_t s, unsigned long long
                              cudaMemcpyDeviceToDevice, s));
     return SWE_OK;
 }
+int LocalTransport::peer_buffers(swe_ctx* c, double* dn[2], double* up[2], int* nloc_dn, swe_status* st) {
+    const int r = rank, n = grp->n;
+    grp->buf[r][0] = c->d_buf[0];
+    grp->buf[r][1] = c->d_buf[1];
+    grp->nloc[r] = c->nloc;
+    GROUP_SYNC();  // every rank has posted its buffers
+    for (int k = 0; k < 2; ++k) {
+        dn[k] = r > 0 ? grp->buf[r - 1][k] : nullptr;
+        up[k] = r + 1 < n ? grp->buf[r + 1][k] : nullptr;
+    }
+    *nloc_dn = r > 0 ? grp->nloc[r - 1] : 0;
+    GROUP_SYNC();
+    return SWE_OK;
+}
 #undef GROUP_SYNC
+
+// What a rank tells its strip neighbours about its state buffers.
+struct PeerInfo {
+    cudaIpcMemHandle_t h[2];
+    double* ptr[2];
+    int pid, device, nloc, ok;
+};
+
+int NcclTransport::peer_buffers(swe_ctx* c, double* dn[2], double* up[2], int* nloc_dn, swe_status* st) {
+    dn[0] = dn[1] = up[0] = up[1] = nullptr;
+    *nloc_dn = 0;
+    PeerInfo mine{};
+    mine.pid = static_cast<int>(getpid());
+    mine.device = c->ex.device;
+    mine.nloc = c->nloc;
+    mine.ok = 1;
+    for (int k = 0; k < 2; ++k) {
+        mine.ptr[k] = c->d_buf[k];
+        if (cudaIpcGetMemHandle(&mine.h[k], c->d_buf[k]) != cudaSuccess) mine.ok = 0;
+    }
+    cudaGetLastError();
+    PeerInfo* d = nullptr;  // [mine, from up, from down]
+    CUDA_TRY(cudaMalloc(&d, 3 * sizeof(PeerInfo)));
+    CUDA_TRY(cudaMemcpyAsync(d, &mine, sizeof mine, cudaMemcpyHostToDevice, c->stream));
+    const int rk = c->ex.rank, nr = c->ex.nranks;
+    const bool has_up = rk + 1 < nr, has_dn = rk > 0;
+    int rc = sendrecv(c, c->stream, has_up ? d : nullptr, has_up ? d + 1 : nullptr, has_dn ? d : nullptr,
+                      has_dn ? d + 2 : nullptr, sizeof(PeerInfo), st);
+    if (rc) {
+        cudaFree(d);
+        return rc;
+    }
+    PeerInfo got[2];
+    CUDA_TRY(cudaMemcpyAsync(got, d + 1, 2 * sizeof(PeerInfo), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    cudaFree(d);
+    auto map = [&](const PeerInfo& q, double* out[2]) {
+        if (!q.ok) return false;
+        if (q.pid == mine.pid) {  // strips of one process (the CLI's cuda:N): in-process peer access
+            if (q.device != c->ex.device) {
+                const cudaError_t e = cudaDeviceEnablePeerAccess(q.device, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+                    cudaGetLastError();
+                    return false;
+                }
+                cudaGetLastError();
+            }
+            out[0] = q.ptr[0];
+            out[1] = q.ptr[1];
+            return true;
+        }
+        for (int k = 0; k < 2; ++k) {  // another process: map its buffers over NVLink
+            void* p = nullptr;
+            if (cudaIpcOpenMemHandle(&p, q.h[k], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                cudaGetLastError();
+                return false;
+            }
+            ipc_opened.push_back(p);
+            out[k] = static_cast<double*>(p);
+        }
+        return true;
+    };
+    bool ok = true;
+    if (has_up) ok = map(got[0], up) && ok;
+    if (has_dn) ok = map(got[1], dn) && ok;
+    if (has_dn) *nloc_dn = got[1].nloc;
+    if (!ok) {  // no peer path to a neighbour: the halo goes through NCCL send/recv
+        dn[0] = dn[1] = up[0] = up[1] = nullptr;
+        *nloc_dn = 0;
+    }
+    return SWE_OK;
+}
 
 int create_transport(swe_ctx* c, const swe_exec& ex, const void* nccl_id, swe_status* st) {
     if (ex.flags & SWE_EXEC_LOCAL_GROUP) {

@@ -106,6 +106,11 @@ struct StepParams {
     unsigned long long* qflag[2];
     const unsigned char* elig;
     unsigned* active;      // active item list (schedule kernel -> step kernel)
+    // fused halo push (strips): the neighbours' state buffers (peer memory);
+    // the epilogue stores its R edge rows straight into their halo rows
+    double* peer_dn[2];    // rank - 1 (its rows nloc_dn .. nloc_dn+R-1 take our rows 0 .. R-1)
+    double* peer_up[2];    // rank + 1 (its rows -R .. -1 take our rows nloc-R .. nloc-1)
+    int p2p, nloc_dn;
     unsigned long long* stats;
     int early;
     int nx, ny;            // global grid

@@ -107,27 +107,36 @@ SCEN = {
 }
 
 
+@pytest.mark.parametrize("halo", ["push", "sendrecv"])
 @pytest.mark.parametrize("nranks", [2, 3, 4])
 @pytest.mark.parametrize("name", sorted(SCEN))
-def test_strips_bit_identical_exact(name, nranks):
+def test_strips_bit_identical_exact(name, nranks, halo, monkeypatch):
+    monkeypatch.setenv("SWE_P2P", "1" if halo == "push" else "0")
     sc = SCEN[name]()
     ref, rr = run_single(sc, True, 60)
     got, rg = run_strips(sc, nranks, True, 60)
     assert rr == rg
     assert same(ref, got)
-    # per step: edge + interior step kernels when strips of >= 32 rows overlap the
-    # halo exchange (one step kernel otherwise), the finalize kernel, and the local
-    # group's allreduce kernel
     rows = sc.spec.ny // nranks
-    assert all(n == (4 if rows >= 32 else 3) * 60 for n in run_strips.launches), run_strips.launches
+    if halo == "push":
+        # fused halo push: one step kernel (it stores its edge rows into the
+        # neighbours' halos), the local group's allreduce kernel, the finalize
+        assert all(n == 3 * 60 for n in run_strips.launches), run_strips.launches
+    else:
+        # send/recv: edge + interior step kernels when strips of >= 32 rows
+        # overlap the halo exchange (one step kernel otherwise), the finalize
+        # kernel, and the local group's allreduce kernel
+        assert all(n == (4 if rows >= 32 else 3) * 60 for n in run_strips.launches), run_strips.launches
     # StepAccounting: R halo rows of h, qx, qy from each neighbour
     R = 2 if sc.phys.nu_art > 0 else 1
     halo = [a["halo_values_exchanged"] for a in run_strips.accounting]
     assert halo == [(1 if r in (0, nranks - 1) else 2) * R * 3 * sc.spec.nx for r in range(nranks)]
 
 
+@pytest.mark.parametrize("halo", ["push", "sendrecv"])
 @pytest.mark.parametrize("name", sorted(SCEN))
-def test_strips_bit_identical_fast(name):
+def test_strips_bit_identical_fast(name, halo, monkeypatch):
+    monkeypatch.setenv("SWE_P2P", "1" if halo == "push" else "0")
     sc = SCEN[name]()
     ref, rr = run_single(sc, False, 60)
     got, rg = run_strips(sc, 4, False, 60)
@@ -135,17 +144,23 @@ def test_strips_bit_identical_fast(name):
     assert same(ref, got)
 
 
-def test_strips_host_step_api():
+@pytest.mark.parametrize("halo", ["push", "sendrecv"])
+def test_strips_host_step_api(halo, monkeypatch):
+    monkeypatch.setenv("SWE_P2P", "1" if halo == "push" else "0")
     sc = S.gen_floodplain(192)
     ref, rr = run_single(sc, True, 30, api="step")
     got, rg = run_strips(sc, 3, True, 30, api="step")
     assert rr == rg and same(ref, got)
-    # step() times the halo exchange and the allreduce of every strip
+    # step() times the halo exchange (none with the fused push: the step kernel
+    # stores the rows) and the allreduce of every strip
     for x in run_strips.exchange:
-        assert x["steps"] == 30 and x["exchange_seconds"] > 0.0 and x["allreduce_seconds"] > 0.0
+        assert x["steps"] == 30 and x["allreduce_seconds"] > 0.0
+        assert (x["exchange_seconds"] == 0.0) if halo == "push" else (x["exchange_seconds"] > 0.0)
 
 
-def test_strips_with_early_exit():
+@pytest.mark.parametrize("halo", ["push", "sendrecv"])
+def test_strips_with_early_exit(halo, monkeypatch):
+    monkeypatch.setenv("SWE_P2P", "1" if halo == "push" else "0")
     sc = S.gen_floodplain(320)
     ref, rr = run_single(sc, True, 60)
     got, rg = run_strips(sc, 2, True, 60, early=True)
@@ -221,11 +236,12 @@ def test_load_initial_on_strips():
         assert bits_equal(fs.qy[r0:r1], ref.qy[r0:r1]) and bits_equal(fs.z[r0:r1], ref.z[r0:r1])
 
 
-def test_strips_mixing_overlapped_and_plain_steps():
+def test_strips_mixing_overlapped_and_plain_steps(monkeypatch):
     """ny = 127 on 4 strips gives bands of 32, 32, 32 and 31 rows: the first
     three overlap their halo exchange, the last does not -- the collectives
     must still pair up (same order on every rank) and the result must equal
-    the single domain."""
+    the single domain (send/recv halo transport)."""
+    monkeypatch.setenv("SWE_P2P", "0")
     sc = S.gen_square_dam(127, 1.0, 0.5)
     ref, rr = run_single(sc, True, 40)
     got, rg = run_strips(sc, 4, True, 40)
