@@ -511,7 +511,10 @@ def main():
 
     strong = None
     if world > 1:
-        strong = strong_scaling_c4(args, world, rank, local, dist, new_id, peak)
+        try:
+            strong = strong_scaling_c4(args, world, rank, local, dist, new_id, peak)
+        except Exception as e:  # the strong-scaling block must not cost the main line
+            strong = {"error": str(e)}
 
     achieved = bpc * cells_local / (ms * 1e-3) / 1e9
     traffic = None
