@@ -277,9 +277,11 @@ int swe_cuda_nccl_unique_id(void* out, swe_status* st);
  * product build returns SWE_ERR_CONFIG. */
 int swe_cuda_debug_guard_check(uint64_t* corrupted_bytes, uint64_t* allocations, swe_status* st);
 /* Runs the step kernel's shared-reciprocal division on device arrays copied
- * from the host: out[k] = a[k] / b[k] as the step computes it (exact != 0:
- * SWE_EXEC_EXACT arithmetic, else the fast-mode quotient).  Used by the
- * parity tests to prove the exact path equals IEEE division. */
+ * from the host: out[k] = a[k] / b[k] as the step computes it (exact = 1:
+ * SWE_EXEC_EXACT arithmetic with ptxas's per-division acceptance test; 2: the
+ * exact step's per-state range test with a[k] as the momentum; 0: the
+ * fast-mode quotient).  Used by the parity tests to prove the exact paths
+ * equal IEEE division. */
 int swe_cuda_selftest_div(const double* a, const double* b, size_t n, int exact, double* out,
                           swe_status* st);
 

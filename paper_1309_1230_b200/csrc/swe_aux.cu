@@ -332,7 +332,12 @@ __global__ void digest_kernel(const double* b, int P, int R, int nx, int nloc, i
 __global__ void selftest_div_kernel(const double* a, const double* b, size_t n, int exact, double* out) {
     for (size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; k < n;
          k += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        if (exact) {
+        if (exact == 2) {  // the per-state range test (SWE_EXACT_STATE_CHECK) with a as the momentum
+            const swe_dev::Recip rc = swe_dev::make_recip(b[k]);
+            out[k] = (swe_dev::h_safe(b[k]) && swe_dev::q_safe(a[k]))
+                         ? swe_dev::quot_checked(a[k], rc, swe_dev::is_zero(a[k]))
+                         : __ddiv_rn(a[k], b[k]);
+        } else if (exact) {
             const swe_dev::Recip rc = swe_dev::make_recip(b[k]);
             out[k] = swe_dev::div_rn(a[k], rc);
         } else {

@@ -327,6 +327,9 @@ struct WarpRing {  // per-warp TMA ring state (warp-uniform)
 #ifndef SWE_ABL
 #define SWE_ABL 0
 #endif
+#ifndef SWE_LATE_SRC
+#define SWE_LATE_SRC 0
+#endif
 #ifndef SWE_EMIT_MASKED
 #define SWE_EMIT_MASKED 0
 #endif
@@ -784,7 +787,11 @@ struct Marcher {
             consume<GI>(out.U, out.zx, out.zy);
             const Rc rcN = A::recip(out.U.h);
             out.FU = A::template flux<MANNING>(out.U, rcN, p.half_g);
-            source_of<EXACT, MANNING && !(SWE_ABL & 16), FLAT, FLAT || XONLY>(out.U, out.FU, rcN, out.zx, out.zy, p.neg_g, p.gnn, out.srx, out.sry);
+            // SWE_LATE_SRC: row b+S's source term (Manning friction) is only
+            // carried to the next iteration; placed after the predictor in the
+            // source so the scheduler overlaps it with the U* chain
+            if constexpr (!SWE_LATE_SRC)
+                source_of<EXACT, MANNING && !(SWE_ABL & 16), FLAT, FLAT || XONLY>(out.U, out.FU, rcN, out.zx, out.zy, p.neg_g, p.gnn, out.srx, out.sry);
 
             // ======== stage 2: predictor at (i, b)   scheme.hpp:100-113
             const CellVec& U = in.U;
@@ -840,6 +847,8 @@ struct Marcher {
             const Flux FS = A::template flux<MANNING>(Us, rcS, p.half_g);
             double ssx, ssy;
             source_of<EXACT, MANNING && !(SWE_ABL & 8), FLAT, FLAT || XONLY>(Us, FS, rcS, in.zx, in.zy, p.neg_g, p.gnn, ssx, ssy);
+            if constexpr (SWE_LATE_SRC)
+                source_of<EXACT, MANNING && !(SWE_ABL & 16), FLAT, FLAT || XONLY>(out.U, out.FU, rcN, out.zx, out.zy, p.neg_g, p.gnn, out.srx, out.sry);
 
             if constexpr (EXACT || !CLASSIC) {
                 // own x face (FWD: east, BWD: west) and y face (b, b+S)   scheme.hpp:153-161

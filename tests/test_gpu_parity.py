@@ -91,6 +91,33 @@ def test_shared_reciprocal_division_is_ieee():
     assert same.all(), (a[~same][:5], b[~same][:5], out[~same][:5], ref[~same][:5])
 
 
+def test_state_checked_division_is_ieee():
+    """SWE_EXACT_STATE_CHECK: inside the range test (|h| in [2^-400, 2^400),
+    momentum 0 or of magnitude in [2^-200, 2^200)) the shared-reciprocal
+    quotient without ptxas's per-division test is the IEEE quotient, signed
+    zeros included; outside it the IEEE division runs -- across the range
+    edges, the specials and random operands."""
+    rng = np.random.Generator(np.random.PCG64(11))
+    n = 1 << 22
+    a = rng.standard_normal(n) * np.exp2(rng.integers(-215, 215, n).astype(np.float64))
+    b = np.abs(rng.standard_normal(n)) * np.exp2(rng.integers(-415, 415, n).astype(np.float64))
+    edges_a = np.array([2.0 ** -200, -(2.0 ** -200), np.nextafter(2.0 ** -200, 0), 2.0 ** 200,
+                        np.nextafter(2.0 ** 200, 0), -(2.0 ** 200), 0.0, -0.0, np.inf, -np.inf, np.nan, 1e-310])
+    edges_b = np.array([2.0 ** -400, np.nextafter(2.0 ** -400, 0), 2.0 ** 400, np.nextafter(2.0 ** 400, 0),
+                        -(2.0 ** -400), 1.0, 3.0, 0.1, 1e-320, np.inf, 0.0, -0.0, np.nan])
+    sa, sb = np.meshgrid(edges_a, edges_b)
+    a = np.concatenate([a, sa.ravel(), a[:1000] * 0.0, -(a[:1000] * 0.0)])
+    b = np.concatenate([b, sb.ravel(), b[:2000]])
+    out = np.empty_like(a)
+    st = abi.swe_status()
+    lib = abi.load_library()
+    assert lib.swe_cuda_selftest_div(abi.dptr(a), abi.dptr(b), a.size, 2, abi.dptr(out), st) == 0
+    with np.errstate(all="ignore"):
+        ref = a / b
+    same = (out.view(np.uint64) == ref.view(np.uint64)) | (np.isnan(out) & np.isnan(ref))
+    assert same.all(), (a[~same][:5], b[~same][:5], out[~same][:5], ref[~same][:5])
+
+
 def test_step_equals_device_resident_advance():
     sc = S.gen_square_dam(200)
     fs = sc.build()
