@@ -830,9 +830,14 @@ constexpr long long kMultiMaxCells = 1 << 20;  // multi-step launches up to 1024
 void guided_chunks(StepParams& p, int rows) {
     const char* env = std::getenv("SWE_GUIDED");
     if (env && env[0] == '0') return;
-    const int c1 = p.chunk, c2 = std::max(8, c1 / 4);
+    int c1 = p.chunk, c2 = std::max(8, c1 / 4);
+    int big_pct = 80;
+    // A/B hooks: first-tier chunk, second-tier chunk, first-tier share of the rows
+    if (const char* e = std::getenv("SWE_CHUNK1")) c1 = p.chunk = std::max(8, std::atoi(e));
+    if (const char* e = std::getenv("SWE_CHUNK2")) c2 = std::max(4, std::atoi(e));
+    if (const char* e = std::getenv("SWE_BIGPCT")) big_pct = std::max(0, std::min(100, std::atoi(e)));
     if (c1 < 32 || rows < 8 * c1) return;
-    const int big = (rows * 4 / 5) / c1;
+    const int big = (rows * big_pct / 100) / c1;
     const int rest = rows - big * c1;
     p.tier_rc = big;
     p.chunk2 = c2;
@@ -973,12 +978,17 @@ int finish_load(swe_ctx* c, double t, swe_status* st) {
     {
         const long long workers = ncta * SWE_STEP_WPB;
         long long ch = units / std::max<long long>(1, workers * 16);
+        // Item heights are multiples of the row group (4 rows per TMA request
+        // in fast mode): a segment then marches whole groups with no tail
+        // iterations (the 8192^2 C3 step: 79-row items 0.830 ms, 80-row
+        // 0.789 ms; 59 -> 64 rows on the flat 8192^2 grid, 0.573 ms)
         if (ch >= 16) {
-            ch = std::min<long long>(128, ch);
+            ch = std::min<long long>(128, (ch + 8) / 16 * 16);
         } else {
             // small grids are latency-bound: the shortest items (>= 4 rows) that
             // still give every worker at most one item (512^2: 28 -> 20 us/step)
             ch = std::max<long long>(4, std::min<long long>(16, (units + workers - 1) / workers));
+            ch = (ch + 3) / 4 * 4;
         }
         // early exit: finer items (32 rows) so the active band is balanced
         // across workers and skipped at a finer grain
