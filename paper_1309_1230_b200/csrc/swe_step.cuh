@@ -531,7 +531,7 @@ struct Marcher {
             double u, v;
             const Rc rc = A::recip(o.h);
             const double c = A::sqrt_(p.g * o.h);
-            A::div2(o.qx, o.qy, rc, u, v);
+            A::template div2<!EARLY>(o.qx, o.qy, rc, u, v);
             sx = fabs(u) + c;
             sy = fabs(v) + c;
         } else if constexpr (SWE_CFL_DEFER) {
@@ -786,7 +786,7 @@ struct Marcher {
             // ======== stage 1: committed row b+S
             consume<GI>(out.U, out.zx, out.zy);
             const Rc rcN = A::recip(out.U.h);
-            out.FU = A::template flux<MANNING>(out.U, rcN, p.half_g);
+            out.FU = A::template flux<MANNING, !EARLY>(out.U, rcN, p.half_g);
             // SWE_LATE_SRC: row b+S's source term (Manning friction) is only
             // carried to the next iteration; placed after the predictor in the
             // source so the scheduler overlaps it with the U* chain
@@ -844,7 +844,7 @@ struct Marcher {
             }
 
             const Rc rcS = A::recip(Us.h);
-            const Flux FS = A::template flux<MANNING>(Us, rcS, p.half_g);
+            const Flux FS = A::template flux<MANNING, !EARLY>(Us, rcS, p.half_g);
             double ssx, ssy;
             source_of<EXACT, MANNING && !(SWE_ABL & 8), FLAT, FLAT || XONLY>(Us, FS, rcS, in.zx, in.zy, p.neg_g, p.gnn, ssx, ssy);
             if constexpr (SWE_LATE_SRC)
@@ -1073,7 +1073,7 @@ struct Marcher {
         consume<0>(A.U, A.zx, A.zy);  // march row 0
         {
             const Rc rc = A::recip(A.U.h);
-            A.FU = A::template flux<MANNING>(A.U, rc, p.half_g);
+            A.FU = A::template flux<MANNING, !EARLY>(A.U, rc, p.half_g);
             source_of<EXACT, MANNING, FLAT, FLAT || XONLY>(A.U, A.FU, rc, A.zx, A.zy, p.neg_g, p.gnn, A.srx, A.sry);
         }
         A.Hyp = {0.0, 0.0, 0.0};
