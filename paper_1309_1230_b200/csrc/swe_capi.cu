@@ -973,6 +973,8 @@ int finish_load(swe_ctx* c, double t, swe_status* st) {
         const int occm = allow ? swe_multi_occupancy(c->exact, c->smooth, vm) : 0;
         c->multi_ok = allow && occm > 0 && static_cast<long long>(nloc) * c->g.nx <= kMultiMaxCells;
         c->ncta_multi = std::max(1, std::min(c->ncta, occm * nsm));
+        if (const char* e = std::getenv("SWE_MULTI_CTAS"))  // A/B hook
+            c->ncta_multi = std::max(1, std::min(std::atoi(e), occm * nsm));
     }
     // dynamic work items: ~16 per worker, 16..128 rows each
     {
