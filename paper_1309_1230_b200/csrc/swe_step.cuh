@@ -336,10 +336,26 @@ struct WarpRing {  // per-warp TMA ring state (warp-uniform)
 #ifndef SWE_CFL_DEFER
 #define SWE_CFL_DEFER 0
 #endif
+// interior windows store all 32 lanes: the two halo lanes' stores go to a
+// pitch-padding column (never read), so the row's epilogue has no branch and
+// the warp no reconvergence point between rows
+// (0 off, 1 every kernel, 2 fast-mode Manning kernels: measured -2.5 % on C3
+// fast, +1 % on the frictionless and flat configs, whose steps are closer to
+// the HBM bound, and +1.8 % on C3 exact)
+#ifndef SWE_EMIT_PAD
+#define SWE_EMIT_PAD 2
+#endif
+// refill the ring right before the next group's wait instead of after the
+// last row of a group: one divergent region (refill + wait) per group
+#ifndef SWE_LATE_PRODUCE
+#define SWE_LATE_PRODUCE 2
+#endif
 
 template <int WPB, bool FWD, bool SMOOTH, int BED, bool MANNING, bool EXACT, bool EARLY>
 struct Marcher {
     static constexpr bool CLASSIC = SWE_FAST_CLASSIC != 0;  // fast-mode corrector form (see iter())
+    static constexpr bool PAD = SWE_EMIT_PAD == 1 || (SWE_EMIT_PAD == 2 && MANNING && !EXACT);
+    static constexpr bool LATE = SWE_LATE_PRODUCE == 1 || (SWE_LATE_PRODUCE == 2 && MANNING && !EXACT);
     static constexpr bool FLAT = BED == 0;
     static constexpr bool XONLY = BED == 2;
     using A = Arith<EXACT>;
@@ -490,7 +506,13 @@ struct Marcher {
     template <int GI>
     __device__ __forceinline__ void consume(CellVec& u, double& zx, double& zy) {
         SWE_DCHECK(ring.d >= 0 && ring.d < D && req < pn);
-        if constexpr (GI == 0) mbar_wait(&bars[ring.d], ring.ph);
+        if constexpr (GI == 0) {
+            if constexpr (LATE) {
+                __syncwarp();  // every lane is done with the released slot
+                produce();
+            }
+            mbar_wait(&bars[ring.d], ring.ph);
+        }
         constexpr int g = FWD ? GI : G - 1 - GI;  // row within the box (boxes ascend in y)
         const double* st = stage + ring.d * SLOT;
         u.h = st[g * 3 * BW + lane + BO];
@@ -514,8 +536,10 @@ struct Marcher {
             ring.ph ^= 1u;
         }
         ++req;
-        __syncwarp();
-        produce();
+        if constexpr (!LATE) {
+            __syncwarp();
+            produce();
+        }
     }
 
     // output cell: guard (K5), CFL (K6), store, ghosts for the next step (K1)
@@ -564,8 +588,8 @@ struct Marcher {
         my = (cfl_ok && sy > my) ? sy : my;
         if constexpr (EARLY) {
             const unsigned long long hb = dbits(o.h), mom = dbits(o.qx) | dbits(o.qy);
-            qo |= hb | mom;
-            qn &= hb & ~mom;
+            qo |= on ? (hb | mom) : 0ull;
+            qn &= on ? (hb & ~mom) : ~0ull;
         }
         if constexpr (TSTORE && SLOT >= 0) {  // stage the row for the warp's TMA store of its group
             constexpr int gr = FWD ? SLOT : G - 1 - SLOT;  // row within the box (boxes ascend in y)
@@ -580,7 +604,8 @@ struct Marcher {
         orow += S * 3 * P;
         SWE_DCHECK(!on || (row == nxt + (static_cast<long long>(rr + R) * 3 * P + (i + SWE_XO)) && rr >= 0 && rr < p.nloc &&
                            i >= 0 && i < p.nx));
-        if (!(TSTORE && SLOT >= 0) && on && !(SWE_ABL & 1)) {
+        // (PAD: a halo lane of an interior window stores to its padding column)
+        if (!(TSTORE && SLOT >= 0) && (on || (PAD && !EDGE)) && !(SWE_ABL & 1)) {
             row[0] = o.h;
             row[P] = o.qx;
             row[2 * P] = o.qy;
@@ -977,7 +1002,7 @@ struct Marcher {
             }
             const int c_row = b;
             if constexpr (!SMOOTH) {
-                if constexpr (SWE_EMIT_MASKED) {
+                if constexpr (SWE_EMIT_MASKED || (PAD && !EDGE)) {
                     if (EMIT) emit<EDGE, SLOT>(C, c_row, out_x);
                 } else {
                     if (EMIT && out_x) emit<EDGE, SLOT>(C, c_row);
@@ -1042,7 +1067,10 @@ struct Marcher {
         const int jlo = p.j0 + sg.ra - R - 1, jhi = p.j0 + sg.rb + R;  // rows the march touches, padded
         // segments with strip edge rows run the edge march too (fused halo push)
         const bool pedge = p.p2p && (sg.ra < R || sg.rb > p.nloc - R);
-        if (xedge || jlo <= 0 || jhi >= p.ny - 1 || pedge) march<true>();
+        const bool edge_march = xedge || jlo <= 0 || jhi >= p.ny - 1 || pedge;
+        if (PAD && !edge_march && !out_x)  // lanes 0 and 31 of an interior window
+            orow = nxt + static_cast<size_t>(r_start + R) * 3 * P + (SWE_XO + p.nx + 2 + (2 * sg.tile + (lane != 0)) % 30);
+        if (edge_march) march<true>();
         else march<false>();
         if (pedge && __any_sync(FULL, pushed)) __threadfence_system();  // the peer stores, system-wide
         if constexpr (!EXACT && SWE_CFL_DEFER) {  // the segment's last pending cell
