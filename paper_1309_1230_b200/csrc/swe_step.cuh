@@ -351,7 +351,9 @@ struct WarpRing {  // per-warp TMA ring state (warp-uniform)
 #define SWE_LATE_PRODUCE 2
 #endif
 
-template <int WPB, bool FWD, bool SMOOTH, int BED, bool MANNING, bool EXACT, bool EARLY>
+// ONE_MARCH: every segment runs the edge march (a superset of the interior
+// one), so the kernel holds one march body per sweep direction
+template <int WPB, bool FWD, bool SMOOTH, int BED, bool MANNING, bool EXACT, bool EARLY, bool ONE_MARCH = false>
 struct Marcher {
     static constexpr bool CLASSIC = SWE_FAST_CLASSIC != 0;  // fast-mode corrector form (see iter())
     static constexpr bool PAD = SWE_EMIT_PAD == 1 || (SWE_EMIT_PAD == 2 && MANNING && !EXACT);
@@ -1068,10 +1070,15 @@ struct Marcher {
         // segments with strip edge rows run the edge march too (fused halo push)
         const bool pedge = p.p2p && (sg.ra < R || sg.rb > p.nloc - R);
         const bool edge_march = xedge || jlo <= 0 || jhi >= p.ny - 1 || pedge;
-        if (PAD && !edge_march && !out_x)  // lanes 0 and 31 of an interior window
-            orow = nxt + static_cast<size_t>(r_start + R) * 3 * P + (SWE_XO + p.nx + 2 + (2 * sg.tile + (lane != 0)) % 30);
-        if (edge_march) march<true>();
-        else march<false>();
+        if constexpr (ONE_MARCH) {
+            march<true>();
+        } else {
+            if (PAD && !edge_march && !out_x)  // lanes 0 and 31 of an interior window
+                orow = nxt + static_cast<size_t>(r_start + R) * 3 * P +
+                       (SWE_XO + p.nx + 2 + (2 * sg.tile + (lane != 0)) % 30);
+            if (edge_march) march<true>();
+            else march<false>();
+        }
         if (pedge && __any_sync(FULL, pushed)) __threadfence_system();  // the peer stores, system-wide
         if constexpr (!EXACT && SWE_CFL_DEFER) {  // the segment's last pending cell
             double sx, sy;
@@ -1390,6 +1397,9 @@ __global__ void __launch_bounds__(256) swe_schedule_kernel(const __grid_constant
 // triple-buffered by step (the buffer of step s+1 is cleared during step s:
 // every CTA stopped reading it before the barrier of step s-1).  A failed
 // step stops every CTA; the host resolves it as after a one-step launch.
+#ifndef SWE_MULTI_ONE_MARCH
+#define SWE_MULTI_ONE_MARCH 1  // multi-step kernels: one march body per direction (instruction cache)
+#endif
 #ifndef SWE_MULTI_STATIC
 #define SWE_MULTI_STATIC 1  // static item assignment in multi-step launches (no per-item atomics)
 #endif
@@ -1416,7 +1426,7 @@ __device__ __forceinline__ void multi_step_body(const StepParams& p, double* sta
                                                 Seg* segq, double* sstage, int lane, int warp, int sel, double dt,
                                                 unsigned* wctr, unsigned long long* red, WarpRing& ring,
                                                 double (*s_red)[WPB]) {
-    using M = Marcher<WPB, FWD, SMOOTH, BED, MANNING, EXACT, false>;
+    using M = Marcher<WPB, FWD, SMOOTH, BED, MANNING, EXACT, false, SWE_MULTI_ONE_MARCH != 0>;
     constexpr unsigned FULL = 0xffffffffu;
     M m{p};
     m.stage = stage;
