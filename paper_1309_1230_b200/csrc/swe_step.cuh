@@ -342,6 +342,9 @@ struct WarpRing {  // per-warp TMA ring state (warp-uniform)
 // (0 off, 1 every kernel, 2 fast-mode Manning kernels: measured -2.5 % on C3
 // fast, +1 % on the frictionless and flat configs, whose steps are closer to
 // the HBM bound, and +1.8 % on C3 exact)
+#ifndef SWE_MULTI_COMPACT
+#define SWE_MULTI_COMPACT 1  // multi-step kernels: two-iteration march trips (see march())
+#endif
 #ifndef SWE_EMIT_PAD
 #define SWE_EMIT_PAD 2
 #endif
@@ -356,6 +359,7 @@ struct WarpRing {  // per-warp TMA ring state (warp-uniform)
 template <int WPB, bool FWD, bool SMOOTH, int BED, bool MANNING, bool EXACT, bool EARLY, bool ONE_MARCH = false>
 struct Marcher {
     static constexpr bool CLASSIC = SWE_FAST_CLASSIC != 0;  // fast-mode corrector form (see iter())
+    static constexpr bool COMPACT = ONE_MARCH && SWE_MULTI_COMPACT != 0;
     static constexpr bool PAD = SWE_EMIT_PAD == 1 || (SWE_EMIT_PAD == 2 && MANNING && !EXACT);
     static constexpr bool LATE = SWE_LATE_PRODUCE == 1 || (SWE_LATE_PRODUCE == 2 && MANNING && !EXACT);
     static constexpr bool FLAT = BED == 0;
@@ -367,6 +371,7 @@ struct Marcher {
     static constexpr int NF = FLAT ? 3 : XONLY ? 4 : 5;  // doubles per cell in the ring
     static constexpr int D = step_stages<EXACT, FLAT, MANNING, EARLY>();
     static constexpr int G = swe_row_group(EXACT, EARLY);
+    static_assert((G & (G - 1)) == 0, "row groups are powers of two");
     static constexpr int BW = swe_box_w(R);   // load box width (32, or 34 for R = 1: see swe_types.h)
     static constexpr int BO = swe_box_off(R); // lane 0's column in the box
     static constexpr int ST_D = swe_pad16(3 * G * BW);         // state box doubles in a slot (padded)
@@ -505,17 +510,19 @@ struct Marcher {
     }
     // Row GI (in march order) of the current group.  Groups never span two
     // segments; the group row of each march iteration is static (see march()).
+    // GI < 0: the group row is the run-time gi (COMPACT marches)
     template <int GI>
-    __device__ __forceinline__ void consume(CellVec& u, double& zx, double& zy) {
+    __device__ __forceinline__ void consume(CellVec& u, double& zx, double& zy, int gi = 0) {
         SWE_DCHECK(ring.d >= 0 && ring.d < D && req < pn);
-        if constexpr (GI == 0) {
+        if constexpr (GI >= 0) gi = GI;
+        if (GI == 0 || (GI < 0 && gi == 0)) {
             if constexpr (LATE) {
                 __syncwarp();  // every lane is done with the released slot
                 produce();
             }
             mbar_wait(&bars[ring.d], ring.ph);
         }
-        constexpr int g = FWD ? GI : G - 1 - GI;  // row within the box (boxes ascend in y)
+        const int g = FWD ? gi : G - 1 - gi;  // row within the box (boxes ascend in y)
         const double* st = stage + ring.d * SLOT;
         u.h = st[g * 3 * BW + lane + BO];
         u.qx = st[g * 3 * BW + BW + lane + BO];
@@ -530,7 +537,7 @@ struct Marcher {
             zx = 0.0;
             zy = 0.0;
         }
-        if constexpr (GI == G - 1) next_group();
+        if (GI == G - 1 || (GI < 0 && gi == G - 1)) next_group();
     }
     __device__ __forceinline__ void next_group() {
         if (++ring.d == D) {
@@ -806,12 +813,12 @@ struct Marcher {
     // EDGE = false: the segment touches no domain edge (interior window, rows
     // clear of j = 0 and j = ny-1), so every boundary test is compiled out.
     template <bool EDGE, bool DO12, bool DO3, bool EMIT, int GI = 0, int SLOT = -1>
-    __device__ __forceinline__ void iter(int k, const Carry& in, Carry& out) {
+    __device__ __forceinline__ void iter(int k, const Carry& in, Carry& out, int gi = 0) {
         const int b = r_start + S * k;  // stage-2 row (local)
         if constexpr (TSTORE && EMIT && SLOT == 0) group_begin();
         if constexpr (DO12) {
             // ======== stage 1: committed row b+S
-            consume<GI>(out.U, out.zx, out.zy);
+            consume<GI>(out.U, out.zx, out.zy, gi);
             const Rc rcN = A::recip(out.U.h);
             out.FU = A::template flux<MANNING, !EARLY>(out.U, rcN, p.half_g);
             // SWE_LATE_SRC: row b+S's source term (Manning friction) is only
@@ -1131,6 +1138,20 @@ struct Marcher {
         const int k_last = SMOOTH ? L : L - 1;
         const int k_first = k;
         // carries enter the steady state in B and alternate (B->A, A->B, ...)
+        if constexpr (COMPACT) {
+            // two iterations per trip with run-time group rows: the
+            // instruction footprint of a small-grid step (4-row items, no
+            // trip runs twice) is two iteration bodies, not G
+            int gi = GI0;
+            for (; k + 1 <= k_last; k += 2) {
+                iter<EDGE, true, true, true, -1>(k, B, A, gi);
+                gi = (gi + 1) & (G - 1);
+                iter<EDGE, true, true, true, -1>(k + 1, A, B, gi);
+                gi = (gi + 1) & (G - 1);
+            }
+            if (k <= k_last) iter<EDGE, true, true, true, -1>(k, B, A, gi);
+            k = k_last + 1;
+        }
         for (; k + G - 1 <= k_last; k += G) {
             iter<EDGE, true, true, true, (GI0 + 0) % G, 0>(k, B, A);
             iter<EDGE, true, true, true, (GI0 + 1) % G, 1>(k + 1, A, B);
