@@ -14,3 +14,6 @@ import json,sys
 d=json.loads(open('$f').read().strip().splitlines()[-1])
 print('$f'.split('/')[-1], round(d['ms_per_step'],5), d.get('roofline',{}).get('frac'), (d.get('other_mode') or {}).get('ms_per_step'), (d.get('clocks') or {}).get('sm_mhz'), (d.get('clocks') or {}).get('reasons'))
 " 2>/dev/null || echo "$f failed"; done
+# launch list of the headline command (cold, serialised: shares, not absolute times)
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/bench_r2/launches_c3.csv python bench.py --steps 20 --warmup 5 --fast --no-cpu-baseline --no-parity --e2e-steps 2 > gpurun_out/bench_r2/launches_c3.log 2>&1
+python tools/launch_summary.py gpurun_out/bench_r2/launches_c3.csv "python bench.py --steps 20 --warmup 5 --fast --no-cpu-baseline --no-parity --e2e-steps 2" > gpurun_out/bench_r2/launches_c3_summary.txt 2>&1
