@@ -361,7 +361,6 @@ struct Marcher {
     static constexpr bool CLASSIC = SWE_FAST_CLASSIC != 0;  // fast-mode corrector form (see iter())
     static constexpr bool COMPACT = ONE_MARCH && SWE_MULTI_COMPACT != 0;
     static constexpr bool PAD = SWE_EMIT_PAD == 1 || (SWE_EMIT_PAD == 2 && MANNING && !EXACT);
-    static constexpr bool LATE = SWE_LATE_PRODUCE == 1 || (SWE_LATE_PRODUCE == 2 && MANNING && !EXACT);
     static constexpr bool FLAT = BED == 0;
     static constexpr bool XONLY = BED == 2;
     using A = Arith<EXACT>;
@@ -370,6 +369,10 @@ struct Marcher {
     static constexpr int S = FWD ? 1 : -1;
     static constexpr int NF = FLAT ? 3 : XONLY ? 4 : 5;  // doubles per cell in the ring
     static constexpr int D = step_stages<EXACT, FLAT, MANNING, EARLY>();
+    // late refill: needs D >= 3, or the refill at a segment's last group never
+    // reaches the next segment's claim (with D = 2 the warp's queue runs dry
+    // and it stops early -- caught by the C3 parity check of a 16-warp build)
+    static constexpr bool LATE = (SWE_LATE_PRODUCE == 1 || (SWE_LATE_PRODUCE == 2 && MANNING && !EXACT)) && D >= 3;
     static constexpr int G = swe_row_group(EXACT, EARLY);
     static_assert((G & (G - 1)) == 0, "row groups are powers of two");
     static constexpr int BW = swe_box_w(R);   // load box width (32, or 34 for R = 1: see swe_types.h)
