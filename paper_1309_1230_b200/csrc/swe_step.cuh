@@ -1278,6 +1278,7 @@ __global__ void __launch_bounds__(WPB * 32, (step_min_blocks<EXACT, BED == 0, MA
         ++m.qhead;
         m.segment(sg);
     }
+    SWE_DCHECK(m.pdone);  // the queue ran dry only after the last claim
     if constexpr (M::TSTORE) {  // this warp's bulk stores complete before the step is finalized
         if (lane == 0) bulk_wait_all();
         __syncwarp();
@@ -1498,6 +1499,7 @@ __device__ __forceinline__ void multi_step_body(const StepParams& p, double* sta
         ++m.qhead;
         m.segment(sg);
     }
+    SWE_DCHECK(m.pdone);
     if constexpr (M::TSTORE) {
         if (lane == 0) bulk_wait_all();
         __syncwarp();
