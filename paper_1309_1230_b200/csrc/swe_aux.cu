@@ -215,9 +215,20 @@ __global__ void initial_kernel(swe_initial ic, double dx, int nx, int nloc, int 
 // K6 exact per-cell scan (timestep.hpp:83-105 / executor.hpp:560-580) and K5
 // guard (timestep.hpp:64-78) over own rows of buffer b.
 __global__ void scan_kernel(const double* b, int P, int R, int nx, int nloc, int j0, double g,
-                            double dx, double dy, double h_min, unsigned long long* out) {
-    // one row per block iteration, columns across the threads (coalesced)
-    unsigned long long bad = 0, minr = 0, guard = 0;
+                            double dx, double dy, double h_min, int cfl, unsigned long long* out) {
+    // one row per block iteration, columns across the threads (coalesced).
+    // cfl = 0: the stability guard only (load, Stepper::stability_guard).
+    // The CFL part needs min over cells of r = min(dx/sx, dy/sy).  Correctly
+    // rounded division by a positive number is monotone, so over the cells
+    // whose quotients are certainly positive and finite (sx, sy within 2^1000
+    // of dx, dy in exponent) that minimum is min(dx / max sx, dy / max sy),
+    // formed on the host from the two maxima; only the other cells take the
+    // per-cell quotients (executor.hpp:560-580), exactly as the reference.
+    // u = qx/h, v = qy/h use the step kernels' shared-reciprocal division
+    // under its range test (IEEE quotients), __ddiv_rn outside it.
+    unsigned long long bad = 0, minr = 0, guard = 0, mxs = 0, mys = 0;
+    const unsigned ex = swe_dev::dexp(dx), ey = swe_dev::dexp(dy);
+    const bool normal_d = ex - 1u < 2046u && ey - 1u < 2046u;  // else every cell takes the per-cell path
     for (int lr = blockIdx.x; lr < nloc; lr += gridDim.x) {
         const double* hr = b + pidx(P, R, lr, 0, 0);
         const unsigned long long row0 = static_cast<unsigned long long>(j0 + lr) * nx;
@@ -228,10 +239,29 @@ __global__ void scan_kernel(const double* b, int P, int R, int nx, int nloc, int
             const bool ok = swe_dev::finite_d(h) && swe_dev::finite_d(qx) && swe_dev::finite_d(qy) &&
                             h >= h_min;
             if (!ok) guard = max(guard, ~idx);
+            if (!cfl) continue;
             // K6 (executor.hpp:560-580)
             const double c = __dsqrt_rn(g * h);
-            const double sx = fabs(__ddiv_rn(qx, h)) + c;
-            const double sy = fabs(__ddiv_rn(qy, h)) + c;
+            double u, v;
+            if (swe_dev::h_safe(h) && swe_dev::q_safe(qx) && swe_dev::q_safe(qy)) {
+                const swe_dev::Recip rc = swe_dev::make_recip(h);
+                u = swe_dev::quot_checked(qx, rc, swe_dev::is_zero(qx));
+                v = swe_dev::quot_checked(qy, rc, swe_dev::is_zero(qy));
+            } else {
+                u = __ddiv_rn(qx, h);
+                v = __ddiv_rn(qy, h);
+            }
+            const double sx = fabs(u) + c;
+            const double sy = fabs(v) + c;
+            const unsigned esx = swe_dev::dexp(sx), esy = swe_dev::dexp(sy);
+            // sx, sy positive normal within 2^1000 of dx, dy: dx/sx, dy/sy in
+            // (2^-1001, 2^1002), positive and finite
+            if (normal_d && sx > 0.0 && sy > 0.0 && esx - 1u < 2046u && esy - 1u < 2046u &&
+                esx + 1000u - ex < 2000u && esy + 1000u - ey < 2000u) {
+                mxs = max(mxs, swe_dev::dbits(sx));
+                mys = max(mys, swe_dev::dbits(sy));
+                continue;
+            }
             const double r = swe_dev::std_min(__ddiv_rn(dx, sx), __ddiv_rn(dy, sy));
             if (!(r > 0.0) || !swe_dev::finite_d(r)) {
                 bad = max(bad, ~idx);
@@ -244,11 +274,15 @@ __global__ void scan_kernel(const double* b, int P, int R, int nx, int nloc, int
         bad = max(bad, __shfl_xor_sync(0xffffffffu, bad, o));
         minr = max(minr, __shfl_xor_sync(0xffffffffu, minr, o));
         guard = max(guard, __shfl_xor_sync(0xffffffffu, guard, o));
+        mxs = max(mxs, __shfl_xor_sync(0xffffffffu, mxs, o));
+        mys = max(mys, __shfl_xor_sync(0xffffffffu, mys, o));
     }
     if ((threadIdx.x & 31) == 0) {
         if (bad) atomicMax(&out[SCAN_BAD], bad);
         if (minr) atomicMax(&out[SCAN_MINR], minr);
         if (guard) atomicMax(&out[SCAN_GUARD], guard);
+        if (mxs) atomicMax(&out[SCAN_MAXSX], mxs);
+        if (mys) atomicMax(&out[SCAN_MAXSY], mys);
     }
 }
 

@@ -337,14 +337,33 @@ int write_ctl(swe_ctx* c, swe_status* st) {
     return SWE_OK;
 }
 
+// min over cells of min(dx/sx, dy/sy) (executor.hpp:560-580) from the scan
+// words: the quotients of the two speed maxima of the cells whose quotients
+// are certainly finite (correctly rounded division is monotone, so the
+// minimum quotient is the quotient of the maximum), and the per-cell minimum
+// of the other cells; +inf for no cells.
+double scan_core(const swe_ctx* c, const unsigned long long sc[SCAN_N]) {
+    auto as_double = [](unsigned long long b) {
+        double d;
+        std::memcpy(&d, &b, 8);
+        return d;
+    };
+    double core = std::numeric_limits<double>::infinity();
+    if (sc[SCAN_MAXSX]) core = std_min(core, c->g.dx / as_double(sc[SCAN_MAXSX]));
+    if (sc[SCAN_MAXSY]) core = std_min(core, c->g.dy / as_double(sc[SCAN_MAXSY]));
+    if (sc[SCAN_MINR]) core = std_min(core, as_double(~sc[SCAN_MINR]));
+    return core;
+}
+
 // Run the exact scan over own rows of buffer `which`; results all-reduced.
-int run_scan(swe_ctx* c, int which, unsigned long long out[SCAN_N], swe_status* st) {
+// cfl = false: the stability guard only.
+int run_scan(swe_ctx* c, int which, unsigned long long out[SCAN_N], swe_status* st, bool cfl = true) {
     CUDA_TRY(cudaMemsetAsync(c->d_scan, 0, SCAN_N * sizeof(unsigned long long), c->stream));
     const size_t n = static_cast<size_t>(c->nloc) * c->g.nx;
     const int blocks = static_cast<int>(std::min<size_t>((n + 255) / 256, 148 * 16));
     scan_kernel<<<std::max(blocks, 1), 256, 0, c->stream>>>(c->d_buf[which], c->pitch, c->R, c->g.nx,
                                                             c->nloc, c->j0, c->ph.g, c->g.dx, c->g.dy,
-                                                            c->pol.h_min, c->d_scan);
+                                                            c->pol.h_min, cfl ? 1 : 0, c->d_scan);
     CUDA_TRY(cudaGetLastError());
     if (c->ex.nranks > 1) {
         int rc = c->tr->allreduce_max(c, c->stream, c->d_scan, SCAN_N, st);
@@ -498,9 +517,7 @@ int resolve(swe_ctx* c, swe_status* st) {
                               static_cast<int>(idx / c->g.nx), h.t_commit,
                               "non-finite wave speed in dt reduction");
         }
-        const unsigned long long b = ~sc[SCAN_MINR];
-        double core;
-        std::memcpy(&core, &b, 8);
+        const double core = scan_core(c, sc);
         const double dt_raw = std_min(c->pol.cfl * core, c->pol.dt_max);
         if (dt_raw < c->pol.dt_min) {
             h.status = SWE_ERR_STEP_COLLAPSE;
@@ -1124,7 +1141,7 @@ EXPORT int swe_cuda_load_initial(swe_ctx* c, const swe_initial* ic, double t, sw
     if (rc) return rc;
     // build_initial_state ends with the stability guard (scenarios.hpp:165-169)
     unsigned long long sc[SCAN_N];
-    rc = run_scan(c, 0, sc, st);
+    rc = run_scan(c, 0, sc, st, false);
     if (rc) return rc;
     if (sc[SCAN_GUARD]) {
         c->loaded = false;
@@ -1223,11 +1240,7 @@ EXPORT int swe_cuda_compute_dt(swe_ctx* c, double t_end, double* dt, swe_status*
         return set_status(st, SWE_ERR_INSTABILITY, static_cast<int>(idx % c->g.nx), static_cast<int>(idx / c->g.nx),
                           c->t, "compute_dt: non-finite wave speed");
     }
-    double core = std::numeric_limits<double>::infinity();
-    if (sc[SCAN_MINR]) {
-        const unsigned long long b = ~sc[SCAN_MINR];
-        std::memcpy(&core, &b, 8);
-    }
+    const double core = scan_core(c, sc);
     const double dt_raw = std_min(c->pol.cfl * core, c->pol.dt_max);  // timestep.hpp:170-177
     if (dt_raw < c->pol.dt_min) {
         int r = set_status(st, SWE_ERR_STEP_COLLAPSE, -1, -1, c->t,
@@ -1243,7 +1256,7 @@ EXPORT int swe_cuda_guard(swe_ctx* c, swe_status* st) {
     if (!c || !c->loaded) return set_status(st, SWE_ERR_CONFIG, -1, -1, 0, "guard: no state loaded");
     CUDA_TRY(cudaSetDevice(c->ex.device));
     unsigned long long sc[SCAN_N];
-    int rc = run_scan(c, c->sel, sc, st);
+    int rc = run_scan(c, c->sel, sc, st, false);
     if (rc) return rc;
     if (!sc[SCAN_GUARD]) return ok_status(st);
     const unsigned long long idx = ~sc[SCAN_GUARD];

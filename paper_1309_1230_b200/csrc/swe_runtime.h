@@ -107,7 +107,7 @@ struct BcSet {
 };
 
 // Scan words (max-combined, like the step reduction).
-enum { SCAN_BAD = 0, SCAN_MINR = 1, SCAN_GUARD = 2, SCAN_DRY = 3, SCAN_N = 4 };
+enum { SCAN_BAD = 0, SCAN_MINR = 1, SCAN_GUARD = 2, SCAN_DRY = 3, SCAN_MAXSX = 4, SCAN_MAXSY = 5, SCAN_N = 6 };
 
 constexpr int kMaxLocalRanks = 16;  // ranks of a local strip group
 struct RedPtrs {
@@ -130,7 +130,7 @@ __global__ void clamp_kernel(const double* zp, int R, int nx, int nloc, int own_
                              double h_min, unsigned* flag);
 __global__ void initial_kernel(swe_initial ic, double dx, int nx, int nloc, int P, int R, double* buf, double* zp);
 __global__ void scan_kernel(const double* b, int P, int R, int nx, int nloc, int j0, double g,
-                            double dx, double dy, double h_min, unsigned long long* out);
+                            double dx, double dy, double h_min, int cfl, unsigned long long* out);
 __global__ void dry_scan_kernel(const double* b, int P, int R, int nx, int ny, int nloc, int j0, double dt,
                                 double dx, double dy, int fwd, int exact, BcSet bs, const double* z_w,
                                 const double* z_e, const double* z_s, const double* z_n, double h_min,
