@@ -362,3 +362,48 @@ def test_bed_variants_match_oracle(bed):
             assert d == dt
         else:
             assert max_err(got.h, got.qx, got.qy, ref.h, ref.qx, ref.qy) <= FAST_TOL
+
+
+def _dt_outcome(st, fs):
+    """compute_dt's value, or the error it raises (type, cell), for one state."""
+    try:
+        st.load(fs)
+        return ("ok", st.compute_dt(math.inf))
+    except Exception as e:  # noqa: BLE001 -- the error itself is compared
+        cell = (e.cell_i(), e.cell_j()) if hasattr(e, "cell_i") else None
+        return (type(e).__name__, cell)
+
+
+@pytest.mark.parametrize("kind", [EXACT, FAST], ids=["exact", "fast"])
+def test_compute_dt_extreme_speeds_match_oracle(kind):
+    # The exact scan folds cells whose CFL quotients are certainly finite into
+    # two speed maxima and takes per-cell quotients only for the others
+    # (swe_aux.cu scan_kernel): both paths, the bad-ratio error and the
+    # reference's std::min NaN asymmetry, against the oracle's compute_dt.
+    spec = GridSpec(40, 24, 1.0, 2.0)
+    j, i = np.mgrid[0:spec.ny, 0:spec.nx].astype(float)
+    base_h = 1.0 + 0.1 * np.sin(0.3 * i) * np.cos(0.2 * j)
+    base_qx = 0.3 * np.cos(0.1 * i)
+    base_qy = -0.2 * np.sin(0.15 * j)
+    pol = StabilityPolicy(cfl=0.45, dt_min=1e-310)
+    cases_ = {
+        "plain": {},
+        "huge_qx": {"qx": (7, 5, 5e302)},          # dx/sx ~ 2e-303: per-cell path, still finite
+        "huge_qy": {"qy": (20, 11, -3e305)},       # dy/sy ~ 7e-306
+        "nan_qy": {"qy": (3, 2, math.nan)},        # std::min(dx/sx, NaN) keeps dx/sx: not bad
+        "nan_qx": {"qx": (9, 9, math.nan)},        # std::min(NaN, dy/sy) is NaN: bad at (9, 9)
+        "inf_qx": {"qx": (30, 4, math.inf)},       # dx/inf = 0: bad
+        "tiny_h": {"h": (12, 6, 1e-310)},          # subnormal depth: huge speeds
+    }
+    for name, mods in cases_.items():
+        h, qx, qy = base_h.copy(), base_qx.copy(), base_qy.copy()
+        for field, (ci, cj, val) in mods.items():
+            {"h": h, "qx": qx, "qy": qy}[field][cj, ci] = val
+        fs = FieldSet(spec, z=np.zeros_like(h), h=h, qx=qx, qy=qy)
+        g = Stepper(spec, PhysicsParams(), pol, BoundarySet(), kind)
+        o = O.OracleStepper(spec, PhysicsParams(), pol, BoundarySet())
+        got, want = _dt_outcome(g, fs), _dt_outcome(o, fs)
+        assert got == want, name
+        if O.ref_available():  # the reference itself, one worker (its first-offender order)
+            r = O.RefStepper(spec, PhysicsParams(), pol, BoundarySet(), O.REF_NAIVE, 1)
+            assert _dt_outcome(r, fs) == want, name
