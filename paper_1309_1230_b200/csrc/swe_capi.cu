@@ -1007,6 +1007,7 @@ int finish_load(swe_ctx* c, double t, swe_status* st) {
             // small grids are latency-bound: the shortest items (>= 4 rows) that
             // still give every worker at most one item (512^2: 28 -> 20 us/step)
             ch = std::max<long long>(4, std::min<long long>(16, (units + workers - 1) / workers));
+            if (const char* e = std::getenv("SWE_SMALL_CHUNK")) ch = std::max(4, std::atoi(e));  // A/B hook
             ch = (ch + 3) / 4 * 4;
         }
         // early exit: finer items (32 rows) so the active band is balanced
