@@ -989,9 +989,7 @@ int finish_load(swe_ctx* c, double t, swe_status* st) {
         const int vm = swe_step_variant(true, c->smooth, c->flat, c->manning, false, c->xonly);
         const int occm = allow ? swe_multi_occupancy(c->exact, c->smooth, vm) : 0;
         c->multi_ok = allow && occm > 0 && static_cast<long long>(nloc) * c->g.nx <= kMultiMaxCells;
-        c->ncta_multi = std::max(1, std::min(c->ncta, occm * nsm));
-        if (const char* e = std::getenv("SWE_MULTI_CTAS"))  // A/B hook
-            c->ncta_multi = std::max(1, std::min(std::atoi(e), occm * nsm));
+        c->occ_multi = occm;
     }
     // dynamic work items: ~16 per worker, 16..128 rows each
     {
@@ -1007,7 +1005,6 @@ int finish_load(swe_ctx* c, double t, swe_status* st) {
             // small grids are latency-bound: the shortest items (>= 4 rows) that
             // still give every worker at most one item (512^2: 28 -> 20 us/step)
             ch = std::max<long long>(4, std::min<long long>(16, (units + workers - 1) / workers));
-            if (const char* e = std::getenv("SWE_SMALL_CHUNK")) ch = std::max(4, std::atoi(e));  // A/B hook
             ch = (ch + 3) / 4 * 4;
         }
         // early exit: finer items (32 rows) so the active band is balanced
@@ -1019,6 +1016,23 @@ int finish_load(swe_ctx* c, double t, swe_status* st) {
         ch = std::min<long long>(ch, nloc);
         c->prm.chunk = static_cast<int>(ch);
         c->prm.nchunks = static_cast<int>((nloc + ch - 1) / ch);
+    }
+    // multi-step launches: the shortest items that give every resident warp
+    // at most one (a warp marches its item's rows serially, one dependent
+    // chain per row: C1 256^2 with 1-row items on 576 CTAs 10.6 -> 8.6 us per
+    // step; C2 keeps 4-row items, its 2368 resident warps being the limit)
+    if (c->multi_ok) {
+        const long long max_warps = static_cast<long long>(c->occ_multi) * nsm * SWE_STEP_WPB;
+        long long mch = std::max<long long>(1, (units + max_warps - 1) / max_warps);
+        if (const char* e = std::getenv("SWE_SMALL_CHUNK")) mch = std::max(1, std::atoi(e));  // A/B hook
+        mch = std::min<long long>(mch, c->prm.chunk);
+        c->multi_chunk = static_cast<int>(mch);
+        c->multi_nchunks = static_cast<int>((nloc + mch - 1) / mch);
+        const long long items = static_cast<long long>(c->ntiles) * c->multi_nchunks;
+        c->ncta_multi = static_cast<int>(std::max<long long>(
+            1, std::min<long long>(static_cast<long long>(c->occ_multi) * nsm, (items + SWE_STEP_WPB - 1) / SWE_STEP_WPB)));
+        if (const char* e = std::getenv("SWE_MULTI_CTAS"))  // A/B hook
+            c->ncta_multi = std::max(1, std::min(std::atoi(e), c->occ_multi * nsm));
     }
     c->prm.row_lo = 0;
     c->prm.row_hi = nloc;
@@ -1349,7 +1363,10 @@ EXPORT int swe_cuda_advance_marked(swe_ctx* c, double t_end, double t_mark, uint
             const int n = static_cast<int>(std::min<uint64_t>(left, 4096));
             CUDA_TRY(cudaMemsetAsync(&c->d_ctl->mwork[0], 0,
                                      sizeof(SweCtl) - offsetof(SweCtl, mwork), c->stream));
-            CUDA_TRY(swe_launch_multi(c->exact, c->smooth, v_multi, c->ncta_multi, c->stream, c->prm, n));
+            StepParams pm = c->prm;  // the multi-step launch's own item height
+            pm.chunk = pm.chunk2 = c->multi_chunk;
+            pm.nchunks = pm.tier_rc = c->multi_nchunks;
+            CUDA_TRY(swe_launch_multi(c->exact, c->smooth, v_multi, c->ncta_multi, c->stream, pm, n));
             c->launches += 1;
         }
         for (int n : use_multi ? std::vector<int>{} : batch_of(launched)) {

@@ -59,6 +59,7 @@ struct swe_ctx {
     int occ = 1;
     bool multi_ok = false;  // small grid: advance() runs many steps per launch (swe_multi_kernel)
     int ncta_multi = 0;
+    int multi_chunk = 0, multi_nchunks = 0, occ_multi = 0;  // item rows of multi-step launches (one item per warp)
     // CUDA graphs of `len` consecutive steps, keyed by (len, parity of the
     // first step, committed selector at the start -- strips only: the halo
     // send/recv addresses depend on it); built on first use
