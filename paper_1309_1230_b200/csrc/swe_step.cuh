@@ -342,9 +342,6 @@ struct WarpRing {  // per-warp TMA ring state (warp-uniform)
 // (0 off, 1 every kernel, 2 fast-mode Manning kernels: measured -2.5 % on C3
 // fast, +1 % on the frictionless and flat configs, whose steps are closer to
 // the HBM bound, and +1.8 % on C3 exact)
-#ifndef SWE_MULTI_COMPACT
-#define SWE_MULTI_COMPACT 1  // multi-step kernels: two-iteration march trips (see march())
-#endif
 #ifndef SWE_EMIT_PAD
 #define SWE_EMIT_PAD 2
 #endif
@@ -352,6 +349,9 @@ struct WarpRing {  // per-warp TMA ring state (warp-uniform)
 // last row of a group: one divergent region (refill + wait) per group
 #ifndef SWE_LATE_PRODUCE
 #define SWE_LATE_PRODUCE 2
+#endif
+#ifndef SWE_MULTI_COMPACT
+#define SWE_MULTI_COMPACT 1  // multi-step kernels: two-iteration march trips (see march())
 #endif
 
 // ONE_MARCH: every segment runs the edge march (a superset of the interior
