@@ -979,6 +979,8 @@ int finish_load(swe_ctx* c, double t, swe_status* st) {
     long long ncta = std::min<long long>(static_cast<long long>(c->occ) * nsm, want);
     // every worker must span at most 7 tiles (MAXSEG = 8 segments)
     ncta = std::max<long long>(ncta, (c->ntiles + 7 * SWE_STEP_WPB - 1) / (7 * SWE_STEP_WPB));
+    if (const char* e = std::getenv("SWE_NCTA"))  // A/B hook: persistent grid size
+        ncta = std::max<long long>(1, std::min<long long>(std::atoll(e), static_cast<long long>(c->occ) * nsm));
     c->ncta = static_cast<int>(ncta);
     c->prm.ncta = c->ncta;
     // multi-step launches for small grids (latency-bound: launch gaps and a
