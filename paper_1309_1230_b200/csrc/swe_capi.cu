@@ -841,6 +841,10 @@ namespace {
 constexpr int kNcclSms = 2;  // SMs left free for NCCL kernels on strips
 constexpr long long kMultiMaxCells = 1 << 20;  // multi-step launches up to 1024^2 cells
 
+#ifndef SWE_ITEMS_PER_WORKER
+#define SWE_ITEMS_PER_WORKER 0  // first-tier work items per persistent worker (warp); 0: by variant
+#endif
+
 // Guided chunking: the first ~80 % of a launch's rows go out in `chunk`-row
 // items, the rest in quarter-size items, so the dynamic queue ends with short
 // items and the last warps finish together.  SWE_GUIDED=0 keeps uniform chunks.
@@ -996,7 +1000,11 @@ int finish_load(swe_ctx* c, double t, swe_status* st) {
     // dynamic work items: ~16 per worker, 16..128 rows each
     {
         const long long workers = ncta * SWE_STEP_WPB;
-        long long ch = units / std::max<long long>(1, workers * 16);
+        // ~16 first-tier items per worker; 20 for the fast sloped-bed kernels
+        // (12 warps/SM: C3 -0.7 %, C3f -0.4 %; the flat and exact kernels at
+        // 16 warps/SM are 0.7-1.4 % slower with it, profiles/r2d_ab_items_per_worker.log)
+        const long long ipw = SWE_ITEMS_PER_WORKER ? SWE_ITEMS_PER_WORKER : (!c->exact && !c->flat) ? 20 : 16;
+        long long ch = units / std::max<long long>(1, workers * ipw);
         // Item heights are multiples of the row group (4 rows per TMA request
         // in fast mode): a segment then marches whole groups with no tail
         // iterations (the 8192^2 C3 step: 79-row items 0.830 ms, 80-row
