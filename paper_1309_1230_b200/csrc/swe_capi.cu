@@ -1000,10 +1000,12 @@ int finish_load(swe_ctx* c, double t, swe_status* st) {
     // dynamic work items: ~16 per worker, 16..128 rows each
     {
         const long long workers = ncta * SWE_STEP_WPB;
-        // ~16 first-tier items per worker; 20 for the fast sloped-bed kernels
-        // (12 warps/SM: C3 -0.7 %, C3f -0.4 %; the flat and exact kernels at
-        // 16 warps/SM are 0.7-1.4 % slower with it, profiles/r2d_ab_items_per_worker.log)
-        const long long ipw = SWE_ITEMS_PER_WORKER ? SWE_ITEMS_PER_WORKER : (!c->exact && !c->flat) ? 20 : 16;
+        // first-tier items per worker: 20 for the fast sloped-bed kernels (12
+        // warps/SM: C3 -0.7 %, C3f -0.4 % against 16), 16 for the fast flat
+        // ones, 12 in exact mode (C3 exact -0.7 %, flat exact -0.4 %; each
+        // alternative measured +0.4-1.4 % on the others:
+        // profiles/r2d_ab_items_per_worker.log)
+        const long long ipw = SWE_ITEMS_PER_WORKER ? SWE_ITEMS_PER_WORKER : c->exact ? 12 : c->flat ? 16 : 20;
         long long ch = units / std::max<long long>(1, workers * ipw);
         // Item heights are multiples of the row group (4 rows per TMA request
         // in fast mode): a segment then marches whole groups with no tail
