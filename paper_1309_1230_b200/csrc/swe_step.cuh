@@ -341,9 +341,10 @@ struct WarpRing {  // per-warp TMA ring state (warp-uniform)
 // interior windows store all 32 lanes: the two halo lanes' stores go to a
 // pitch-padding column (never read), so the row's epilogue has no branch and
 // the warp no reconvergence point between rows
-// (0 off, 1 every kernel, 2 fast-mode Manning kernels: measured -2.5 % on C3
-// fast, +1 % on the frictionless and flat configs, whose steps are closer to
-// the HBM bound, and +1.8 % on C3 exact)
+// (0 off, 1 every kernel, 2 the fast Manning and the exact frictionless
+// kernels: measured -2.5 % on C3 fast, -0.8 % on C3f / flat exact; +1 % on
+// the fast frictionless and flat configs, whose steps are closer to the HBM
+// bound, +2 % on C3 exact and +2.6 % on C5)
 #ifndef SWE_EMIT_PAD
 #define SWE_EMIT_PAD 2
 #endif
@@ -364,7 +365,8 @@ template <int WPB, bool FWD, bool SMOOTH, int BED, bool MANNING, bool EXACT, boo
 struct Marcher {
     static constexpr bool CLASSIC = SWE_FAST_CLASSIC != 0;  // fast-mode corrector form (see iter())
     static constexpr bool COMPACT = ONE_MARCH && SWE_MULTI_COMPACT != 0;
-    static constexpr bool PAD = SWE_EMIT_PAD == 1 || (SWE_EMIT_PAD == 2 && MANNING && !EXACT);
+    static constexpr bool PAD =
+        SWE_EMIT_PAD == 1 || (SWE_EMIT_PAD == 2 && !EARLY && (EXACT ? !MANNING : MANNING));
     static constexpr bool FLAT = BED == 0;
     static constexpr bool XONLY = BED == 2;
     using A = Arith<EXACT>;
