@@ -268,6 +268,13 @@ int32_t swe_cuda_halo_rows(const swe_ctx* ctx);
 int swe_cuda_state_digest(swe_ctx* ctx, uint64_t* digest, swe_status* st);
 
 /* ---- multi-GPU plumbing ---------------------------------------------- */
+/* The rows [*row_begin, *row_end) that swe_cuda_create gives `rank` of
+ * `nranks` strips: the reference's partition_scanlines (executor.hpp:189-208;
+ * contiguous bands, sizes differ by <= 1, larger first) with the decomposed
+ * executor's >= 4-row band rule; the same errors as create.  Host only (no
+ * CUDA call), so the strip protocol can be checked without a GPU. */
+int swe_cuda_strip_rows(int32_t ny, int32_t nranks, int32_t rank, int32_t* row_begin, int32_t* row_end,
+                        swe_status* st);
 /* ncclGetUniqueId into out[SWE_NCCL_ID_BYTES] (rank 0 broadcasts it). */
 int swe_cuda_nccl_unique_id(void* out, swe_status* st);
 

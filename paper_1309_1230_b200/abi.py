@@ -128,6 +128,8 @@ SIGNATURES = {
     "swe_cuda_state_digest": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(swe_status)]),
     "swe_cuda_debug_guard_check": (C.c_int, [C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(swe_status)]),
     "swe_cuda_nccl_unique_id": (C.c_int, [C.c_void_p, ST]),
+    "swe_cuda_strip_rows": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                      ST]),
     "swe_cuda_version": (C.c_char_p, []),
     "swe_cuda_launch_count": (C.c_uint64, [C.c_void_p]),
     "swe_cuda_selftest_div": (C.c_int, [DP, DP, C.c_size_t, C.c_int, DP, ST]),

@@ -626,6 +626,30 @@ EXPORT const char* swe_cuda_version(void) { return "swe-b200 1.0 (sm_100a, ABI 1
 
 EXPORT int swe_cuda_nccl_unique_id(void* out, swe_status* st) { return nccl_unique_id(out, st); }
 
+// The row strip of `rank` (executor.hpp:189-208 partition_scanlines, with the
+// decomposed executor's >= 4-row band rule); host only, no CUDA call.
+EXPORT int swe_cuda_strip_rows(int32_t ny, int32_t nranks, int32_t rank, int32_t* row_begin, int32_t* row_end,
+                               swe_status* st) {
+    if (!row_begin || !row_end) return set_status(st, SWE_ERR_CONFIG, -1, -1, 0, "strip_rows: null output");
+    if (nranks < 1) return set_status(st, SWE_ERR_CONFIG, -1, -1, 0, "partition_scanlines: workers must be >= 1");
+    if (rank < 0 || rank >= nranks)
+        return set_status(st, SWE_ERR_CONFIG, -1, -1, 0, "exec: rank %d outside [0, %d)", rank, nranks);
+    if (ny < nranks)
+        return set_status(st, SWE_ERR_CONFIG, -1, -1, 0,
+                          "partition_scanlines: %d workers need at least as many rows, grid has %d", nranks, ny);
+    const auto bands = partition_scanlines(ny, nranks);
+    if (nranks > 1)
+        for (const auto& b : bands)
+            if (b.second - b.first < 4)
+                return set_status(st, SWE_ERR_CONFIG, -1, -1, 0,
+                                  "executor: decomposed bands need at least 4 rows; %d workers on %d rows "
+                                  "leaves a band with %d",
+                                  nranks, ny, b.second - b.first);
+    *row_begin = bands[rank].first;
+    *row_end = bands[rank].second;
+    return ok_status(st);
+}
+
 EXPORT int swe_cuda_create(const swe_grid* grid, const swe_physics* phys, const swe_policy* pol,
                            const swe_boundary_set* bnd, const swe_exec* exec, swe_ctx** out,
                            swe_status* st) {
@@ -637,18 +661,8 @@ EXPORT int swe_cuda_create(const swe_grid* grid, const swe_physics* phys, const 
     if (ex.nranks < 1) ex.nranks = 1;
     if (ex.rank < 0 || ex.rank >= ex.nranks)
         return set_status(st, SWE_ERR_CONFIG, -1, -1, 0, "exec: rank %d outside [0, %d)", ex.rank, ex.nranks);
-    if (grid->ny < ex.nranks)
-        return set_status(st, SWE_ERR_CONFIG, -1, -1, 0,
-                          "partition_scanlines: %d workers need at least as many rows, grid has %d", ex.nranks,
-                          grid->ny);
-    auto bands = partition_scanlines(grid->ny, ex.nranks);
-    if (ex.nranks > 1)
-        for (auto& b : bands)
-            if (b.second - b.first < 4)
-                return set_status(st, SWE_ERR_CONFIG, -1, -1, 0,
-                                  "executor: decomposed bands need at least 4 rows; %d workers on %d rows "
-                                  "leaves a band with %d",
-                                  ex.nranks, grid->ny, b.second - b.first);
+    int32_t band_b = 0, band_e = 0;
+    if (int rc = swe_cuda_strip_rows(grid->ny, ex.nranks, ex.rank, &band_b, &band_e, st)) return rc;
     CUDA_TRY(cudaSetDevice(ex.device));
 
     swe_ctx* c = new swe_ctx();
@@ -666,8 +680,8 @@ EXPORT int swe_cuda_create(const swe_grid* grid, const swe_physics* phys, const 
     c->halo_x = c->R;
     if (const char* hx = std::getenv("SWE_DEBUG_HALO_ROWS"))  // test hook (halo mutation)
         c->halo_x = std::max(0, std::min(c->R, std::atoi(hx)));
-    c->j0 = bands[ex.rank].first;
-    c->nloc = bands[ex.rank].second - bands[ex.rank].first;
+    c->j0 = band_b;
+    c->nloc = band_e - band_b;
     const int out_w = SWE_TILE_W(c->R);
     c->ntiles = (grid->nx + out_w - 1) / out_w;
     // columns touched: the last window's load box ends at ntiles*TW - R + SWE_XO + 33

@@ -413,6 +413,17 @@ class Stepper:
         return d.value
 
 
+def strip_rows(ny: int, nranks: int, rank: int):
+    """The rows (begin, end) libswe_cuda gives `rank` of `nranks` strips
+    (swe_cuda_strip_rows: partition_scanlines + the >= 4-row band rule).  Host
+    only: callable without a GPU."""
+    b, e = C.c_int32(), C.c_int32()
+    st = abi.swe_status()
+    if abi.load_library().swe_cuda_strip_rows(int(ny), int(nranks), int(rank), C.byref(b), C.byref(e), C.byref(st)):
+        raise_status(st)
+    return b.value, e.value
+
+
 def partition_scanlines(ny: int, workers: int):
     """executor.hpp:189-208: contiguous bands, sizes differ by <= 1, larger first."""
     if workers < 1:

@@ -6,6 +6,8 @@ import os
 import re
 import subprocess
 
+import pytest
+
 from paper_1309_1230_b200 import abi
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -92,3 +94,14 @@ def test_create_validates_like_the_reference_without_a_gpu():
     assert lib.swe_cuda_create(C.byref(g10), C.byref(p), C.byref(po), C.byref(b), C.byref(strips), C.byref(ctx),
                                C.byref(st)) == abi.SWE_ERR_CONFIG
     assert b"at least 4 rows" in st.msg
+
+
+def test_strip_rows_match_partition_scanlines_and_create_errors():
+    # host-only C-ABI entry (no GPU): the strips swe_cuda_create assigns
+    from paper_1309_1230_b200.stepper import ConfigError, partition_scanlines, strip_rows
+    for ny, n in [(10, 1), (10, 2), (17, 3), (8192, 8), (35, 4), (32768, 8)]:
+        assert [strip_rows(ny, n, r) for r in range(n)] == partition_scanlines(ny, n)
+    for args, msg in [((3, 4, 0), "need at least as many rows"), ((10, 3, 0), "at least 4 rows"),
+                      ((10, 2, 2), "outside"), ((10, 0, 0), "workers must be >= 1")]:
+        with pytest.raises(ConfigError, match=msg):
+            strip_rows(*args)

@@ -7,7 +7,8 @@ the strip neighbours every step and all-reduces the CFL minimum
 (gloo) between two processes, each stepping its strip (plus halo) with the CPU
 oracle, and checks that the assembled result is bit-identical to the
 single-domain run — the decomposition contract the reference's decomposed
-executor pins (test_executor.cpp:151-167)."""
+executor pins (test_executor.cpp:151-167).  Each rank takes its rows from
+libswe_cuda itself (swe_cuda_strip_rows, host only)."""
 import math
 import os
 import socket
@@ -21,7 +22,7 @@ import torch.multiprocessing as mp
 from oracle import oracle as O
 from paper_1309_1230_b200 import scenarios as S
 from paper_1309_1230_b200.stepper import (BoundaryKind, BoundarySet, FieldSet, GridSpec, PhysicsParams,
-                                          StabilityPolicy, partition_scanlines)
+                                          StabilityPolicy, partition_scanlines, strip_rows)
 
 HALO = 3  # committed rows beyond the strip that a one-step redundant update needs (2 with smoothing + 1)
 
@@ -53,7 +54,11 @@ def _worker(rank, world, port, nu, steps, out):
     bounds = BoundarySet(BoundaryKind.transmissive(), BoundaryKind.wall(), BoundaryKind.fixed_eta(1.0),
                          BoundaryKind.inflow(0.1, 1.0))
     phys, pol = PhysicsParams(nu_art=nu), StabilityPolicy(cfl=0.45)
-    j0, j1 = partition_scanlines(spec.ny, world)[rank]
+    # this rank's strip as libswe_cuda assigns it (swe_cuda_strip_rows, the
+    # partition swe_cuda_create uses: host only, no GPU needed), checked
+    # against the reference's partition_scanlines
+    j0, j1 = strip_rows(spec.ny, world, rank)
+    assert (j0, j1) == partition_scanlines(spec.ny, world)[rank]
     a, b = max(j0 - HALO, 0), min(j1 + HALO, spec.ny)
     sub = GridSpec(spec.nx, b - a, spec.dx, spec.dy)
     h, qx, qy, z = (x[a:b].copy() for x in (ic.h, ic.qx, ic.qy, ic.z))
