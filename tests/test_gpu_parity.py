@@ -407,3 +407,47 @@ def test_compute_dt_extreme_speeds_match_oracle(kind):
         if O.ref_available():  # the reference itself, one worker (its first-offender order)
             r = O.RefStepper(spec, PhysicsParams(), pol, BoundarySet(), O.REF_NAIVE, 1)
             assert _dt_outcome(r, fs) == want, name
+
+
+@pytest.mark.parametrize("nx,ny", [(31, 17), (61, 33), (95, 200), (130, 67), (257, 129), (300, 41)])
+def test_odd_shapes_channel_flood_match_oracle(nx, ny):
+    # Window / item geometry edge cases for every kernel family the channel
+    # flood selects (sloped bed along x, Manning friction: the fast kernels
+    # with the padding-column epilogue and the late ring refill; the exact
+    # ones): widths that leave partial windows, heights that leave partial
+    # items and row groups.  Exact mode within the Manning tolerance (std::pow),
+    # fast mode within FAST_TOL, dt_next alike.
+    base = S.gen_channel_flood(64)
+    spec = GridSpec(nx, ny, 1.0, 1.0)
+    slope = 0.5 / (nx - 1)
+    i = np.arange(nx, dtype=float)[None, :].repeat(ny, axis=0)
+    z = slope * (nx - 1 - i)
+    fs = FieldSet(spec, z=z, h=np.maximum(1.0 - z, 0.05) + 0.01 * np.sin(0.2 * i), qx=np.zeros_like(z),
+                  qy=np.zeros_like(z))
+    ora = O.OracleStepper(spec, base.phys, base.pol, base.bounds)
+    ora.load(fs)
+    dt = ora.compute_dt(math.inf)
+    d_o = dt
+    for k in range(25):
+        d_o = ora.step(d_o, k).dt_next
+    ref = ora.state()
+    for kind in (EXACT, FAST):
+        st = Stepper(spec, base.phys, base.pol, base.bounds, kind)
+        st.load(fs)
+        d = st.compute_dt(math.inf)
+        assert d == dt
+        for k in range(25):
+            d = st.step(d, k).dt_next
+        got = st.state()
+        assert max_err(got.h, got.qx, got.qy, ref.h, ref.qx, ref.qy) <= (MANNING_TOL if kind is EXACT else FAST_TOL)
+        assert abs(d - d_o) <= 1e-12 * d_o
+        # the same 25 steps through the device-resident loop (multi-step
+        # launches at these sizes: one march body, run-time group rows, their
+        # own item heights, grid sync)
+        sa = Stepper(spec, base.phys, base.pol, base.bounds, kind)
+        sa.load(fs)
+        r = sa.advance(1e18, 0, dt, 25)
+        assert r.steps == 25
+        ga = sa.state()
+        assert bits_equal(ga.h, got.h) and bits_equal(ga.qx, got.qx) and bits_equal(ga.qy, got.qy)
+        assert r.dt_next == d
