@@ -451,3 +451,55 @@ def test_odd_shapes_channel_flood_match_oracle(nx, ny):
         ga = sa.state()
         assert bits_equal(ga.h, got.h) and bits_equal(ga.qx, got.qx) and bits_equal(ga.qy, got.qy)
         assert r.dt_next == d
+
+
+@pytest.mark.parametrize("nx,ny", [(61, 33), (130, 67), (257, 129)])
+@pytest.mark.parametrize("exact", [True, False], ids=["exact", "fast"])
+def test_odd_shapes_smoothing_and_early_exit(nx, ny, exact):
+    # Smoothing (R = 2: 28-column windows, 5-row stencil) and wet/dry early
+    # exit on odd shapes: a square dam with a quiet right half.  Smoothing vs
+    # the oracle; early exit bit-identical to the non-skipping kernel, both
+    # through step() and advance().
+    spec = GridSpec(nx, ny, 1.0, 1.0)
+    i = np.arange(nx, dtype=float)[None, :].repeat(ny, axis=0)
+    h = np.where(i < nx // 3, 1.0, 0.6)
+    fs = FieldSet(spec, z=np.zeros_like(h), h=h, qx=np.zeros_like(h), qy=np.zeros_like(h))
+    bounds = BoundarySet.all(BoundaryKind.wall())
+    pol = StabilityPolicy(cfl=0.45)
+    # smoothing
+    phys = PhysicsParams(nu_art=0.05)
+    ora = O.OracleStepper(spec, phys, pol, bounds)
+    ora.load(fs)
+    d_o = dt = ora.compute_dt(math.inf)
+    for k in range(20):
+        d_o = ora.step(d_o, k).dt_next
+    ref = ora.state()
+    st = Stepper(spec, phys, pol, bounds, ExecutorKind(exact=exact))
+    st.load(fs)
+    d = st.compute_dt(math.inf)
+    assert d == dt
+    for k in range(20):
+        d = st.step(d, k).dt_next
+    got = st.state()
+    if exact:
+        assert bits_equal(got.h, ref.h) and bits_equal(got.qx, ref.qx) and bits_equal(got.qy, ref.qy) and d == d_o
+    else:
+        assert max_err(got.h, got.qx, got.qy, ref.h, ref.qx, ref.qy) <= FAST_TOL
+    # early exit (no smoothing) against the non-skipping kernel
+    phys = PhysicsParams()
+    runs = []
+    for early in (False, True):
+        for api in ("step", "advance"):
+            s2 = Stepper(spec, phys, pol, bounds, ExecutorKind(exact=exact, early_exit=early))
+            s2.load(fs)
+            d2 = s2.compute_dt(math.inf)
+            if api == "step":
+                for k in range(40):
+                    d2 = s2.step(d2, k).dt_next
+            else:
+                d2 = s2.advance(1e18, 0, d2, 40).dt_next
+            runs.append((s2.state(), d2))
+    base, d_base = runs[0]
+    for got, d2 in runs[1:]:
+        assert bits_equal(got.h, base.h) and bits_equal(got.qx, base.qx) and bits_equal(got.qy, base.qy)
+        assert d2 == d_base
