@@ -100,10 +100,17 @@ def _rect_channel():
     return sc
 
 
+def _rect_channel_manning():
+    sc = S.gen_channel_flood(300, manning_n=0.035)
+    sc.spec = GridSpec(300, 181, 1.0, 1.0)
+    return sc
+
+
 SCEN = {
     "dam256": lambda: S.gen_square_dam(256, 1.0, 0.5),                       # R = 1, walls
     "floodplain256": lambda: S.gen_floodplain(256),                          # R = 2 (smoothing)
     "channel_rect": _rect_channel,                                           # sloped bed, inflow / fixed eta
+    "channel_manning_rect": _rect_channel_manning,                           # + Manning: the padding-column epilogue
 }
 
 
