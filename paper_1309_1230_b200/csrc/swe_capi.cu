@@ -580,25 +580,45 @@ int destroy_graphs(swe_ctx* c) {
 
 // The graph of `len` steps whose first step has sweep parity `parity` and
 // finds the committed selector at `sel` (only strips depend on sel).
+// A step graph that cannot be captured or instantiated (e.g. a transport's
+// collectives refusing capture on some system) is not an error of the run:
+// get_graph returns kGraphUnavailable once, and advance() launches the steps
+// plainly from then on (same kernels, same order).
+constexpr int kGraphUnavailable = -100;
+
 int get_graph(swe_ctx* c, int len, int parity, int sel, swe_ctx::Graph** out, swe_status* st) {
     if (c->ex.nranks == 1) sel = 0;  // one rank: the kernels read the selector on the device
     const int key = (len << 2) | (parity << 1) | sel;
     auto it = c->graphs.find(key);
     if (it == c->graphs.end()) {
         const unsigned long long before = c->launches;
-        cudaGraph_t gph;
+        cudaGraph_t gph = nullptr;
         CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
         int rc = SWE_OK;
         for (int k = 0; k < len && rc == SWE_OK; ++k)
             rc = enqueue_step(c, ((parity + k) % 2) == 0, (sel + k + 1) & 1, st);
         cudaError_t e = cudaStreamEndCapture(c->stream, &gph);
-        if (rc) return rc;
-        CUDA_TRY(e);
+        const unsigned long long captured = c->launches - before;
+        c->launches = before;  // captured (or discarded), not launched
+        if (rc) {
+            if (gph) cudaGraphDestroy(gph);
+            return rc;
+        }
         swe_ctx::Graph g;
-        CUDA_TRY(cudaGraphInstantiate(&g.exec, gph, 0));
-        cudaGraphDestroy(gph);
-        g.kernels = c->launches - before;
-        c->launches = before;  // captured, not launched
+        if (e == cudaSuccess) e = cudaGraphInstantiate(&g.exec, gph, 0);
+        if (const char* f = std::getenv("SWE_DEBUG_GRAPH_FAIL"); f && f[0] == '1' && e == cudaSuccess) {
+            cudaGraphExecDestroy(g.exec);  // test hook: the fallback below
+            e = cudaErrorStreamCaptureUnsupported;
+        }
+        if (gph) cudaGraphDestroy(gph);
+        if (e != cudaSuccess) {
+            cudaGetLastError();  // capture errors are not sticky
+            std::fprintf(stderr, "swe-b200: CUDA graph of %d steps unavailable (%s); launching steps without graphs\n",
+                         len, cudaGetErrorString(e));
+            c->graph_failed = true;
+            return kGraphUnavailable;
+        }
+        g.kernels = captured;
         it = c->graphs.emplace(key, g).first;
     }
     *out = &it->second;
@@ -1354,7 +1374,7 @@ EXPORT int swe_cuda_advance_marked(swe_ctx* c, double t_end, double t_mark, uint
     std::memset(h.red, 0, sizeof h.red);
     int rc = write_ctl(c, st);
     if (rc) return rc;
-    const bool use_graph = !(c->ex.flags & SWE_EXEC_NO_GRAPH) && (!c->tr || c->tr->capturable());
+    bool use_graph = !(c->ex.flags & SWE_EXEC_NO_GRAPH) && (!c->tr || c->tr->capturable()) && !c->graph_failed;
     // small grids, one rank, no early exit: many steps per cooperative launch
     // (swe_multi_kernel) instead of one launch per step
     const int v_multi = swe_step_variant(true, c->smooth, c->flat, c->manning, false, c->xonly);
@@ -1371,6 +1391,10 @@ EXPORT int swe_cuda_advance_marked(swe_ctx* c, double t_end, double t_mark, uint
         for (int n : batch_of(0)) {
             swe_ctx::Graph* g;
             rc = get_graph(c, n, static_cast<int>(par % 2), static_cast<int>(sl % 2), &g, st);
+            if (rc == kGraphUnavailable) {
+                use_graph = false;
+                break;
+            }
             if (rc) return rc;
             par += n;
             sl += n;
@@ -1396,10 +1420,13 @@ EXPORT int swe_cuda_advance_marked(swe_ctx* c, double t_end, double t_mark, uint
             c->launches += 1;
         }
         for (int n : use_multi ? std::vector<int>{} : batch_of(launched)) {
+            swe_ctx::Graph* g = nullptr;
             if (use_graph) {
-                swe_ctx::Graph* g;
                 rc = get_graph(c, n, static_cast<int>(par % 2), static_cast<int>(sl % 2), &g, st);
-                if (rc) return rc;
+                if (rc == kGraphUnavailable) use_graph = false;
+                else if (rc) return rc;
+            }
+            if (use_graph) {
                 CUDA_TRY(cudaGraphLaunch(g->exec, c->stream));
                 c->launches += g->kernels;
             } else {

@@ -58,6 +58,7 @@ struct swe_ctx {
     int ncta = 0;
     int occ = 1;
     bool multi_ok = false;  // small grid: advance() runs many steps per launch (swe_multi_kernel)
+    bool graph_failed = false;  // a step-graph capture failed: advance() launches plainly from then on
     int ncta_multi = 0;
     int multi_chunk = 0, multi_nchunks = 0, occ_multi = 0;  // item rows of multi-step launches (one item per warp)
     // CUDA graphs of `len` consecutive steps, keyed by (len, parity of the

@@ -503,3 +503,22 @@ def test_odd_shapes_smoothing_and_early_exit(nx, ny, exact):
     for got, d2 in runs[1:]:
         assert bits_equal(got.h, base.h) and bits_equal(got.qx, base.qx) and bits_equal(got.qy, base.qy)
         assert d2 == d_base
+
+
+def test_graph_capture_failure_falls_back_to_plain_launches(monkeypatch, capfd):
+    # a step graph that cannot be captured (SWE_DEBUG_GRAPH_FAIL simulates it)
+    # is not a run error: advance() launches the same steps without graphs
+    sc = S.gen_channel_flood(1100, manning_n=0.035)  # > kMultiMaxCells: per-step launches
+    fs = sc.build()
+    out = []
+    for fail in ("0", "1"):
+        monkeypatch.setenv("SWE_DEBUG_GRAPH_FAIL", fail)
+        st = Stepper(sc.spec, sc.phys, sc.pol, sc.bounds, FAST)
+        st.load(fs)
+        r = st.advance(1e18, 0, math.nan, 20)
+        out.append((st.state(), r.steps, r.dt_next, st.launch_count()))
+        st.close()
+    (a, na, da, la), (b, nb, db, lb) = out
+    assert na == nb == 20 and da == db and la == lb == 20
+    assert bits_equal(a.h, b.h) and bits_equal(a.qx, b.qx) and bits_equal(a.qy, b.qy)
+    assert "launching steps without graphs" in capfd.readouterr().err
