@@ -585,6 +585,7 @@ int destroy_graphs(swe_ctx* c) {
 // get_graph returns kGraphUnavailable once, and advance() launches the steps
 // plainly from then on (same kernels, same order).
 constexpr int kGraphUnavailable = -100;
+constexpr long long kL2BandBytes = 48ll << 20;  // rows in flight of the persistent step (see finish_load)
 
 int get_graph(swe_ctx* c, int len, int parity, int sel, swe_ctx::Graph** out, swe_status* st) {
     if (c->ex.nranks == 1) sel = 0;  // one rank: the kernels read the selector on the device
@@ -1046,7 +1047,18 @@ int finish_load(swe_ctx* c, double t, swe_status* st) {
         // iterations (the 8192^2 C3 step: 79-row items 0.830 ms, 80-row
         // 0.789 ms; 59 -> 64 rows on the flat 8192^2 grid, 0.573 ms)
         if (ch >= 16) {
-            ch = std::min<long long>(128, (ch + 8) / 16 * 16);
+            // L2 residency: items go out row-chunk-major, so the rows in flight
+            // are about one chunk across the whole width; kept within ~48 MB of
+            // the 126 MB L2 the neighbouring windows' halo columns and the next
+            // chunk's halo rows are L2 hits (C4 32768^2: 128-row items 9.9 ms,
+            // 64-row 8.75 ms, profiles/r2d_ab_c4_item_rows.log)
+            // (fast mode: exact mode, compute-heavier, keeps 128-row items:
+            // 64 rows cost it 1-2 % on C4)
+            const long long cell_b = 24 + (c->flat ? 0 : c->xonly ? 8 : 16);  // state + slope bytes
+            const long long cap = c->exact ? 128
+                                           : std::max<long long>(16, std::min<long long>(
+                                                 128, (kL2BandBytes / (static_cast<long long>(nx) * cell_b)) / 16 * 16));
+            ch = std::min<long long>(cap, (ch + 8) / 16 * 16);
         } else {
             // small grids are latency-bound: the shortest items (>= 4 rows) that
             // still give every worker at most one item (512^2: 28 -> 20 us/step)
