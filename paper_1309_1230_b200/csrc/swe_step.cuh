@@ -355,6 +355,9 @@ struct WarpRing {  // per-warp TMA ring state (warp-uniform)
 #ifndef SWE_LATE_PRODUCE
 #define SWE_LATE_PRODUCE 2
 #endif
+#ifndef SWE_MIRROR_BWD
+#define SWE_MIRROR_BWD 1  // backward sweeps take their items top-down (see prod_seg)
+#endif
 #ifndef SWE_MULTI_COMPACT
 #define SWE_MULTI_COMPACT 1  // multi-step kernels: two-iteration march trips (see march())
 #endif
@@ -490,6 +493,17 @@ struct Marcher {
         } else {
             sg.ra = p.row_lo + p.tier_rc * p.chunk + (rc - p.tier_rc) * p.chunk2;
             sg.rb = min(sg.ra + p.chunk2, p.row_hi);
+        }
+        if constexpr (SWE_MIRROR_BWD && !FWD && !EARLY) {
+            // backward sweeps hand out the rows top-down (the same items,
+            // mirrored): the forward sweep before wrote the top rows last, so
+            // the first reads of this step hit what is still in L2, and the
+            // next forward sweep starts on the rows this one wrote last
+            if (p.row_gap == 0) {
+                const int a = sg.ra, b = sg.rb;
+                sg.ra = p.row_lo + p.row_hi - b;
+                sg.rb = p.row_lo + p.row_hi - a;
+            }
         }
         SWE_DCHECK(sg.tile >= 0 && sg.tile < p.ntiles && sg.ra >= p.row_lo && sg.ra < sg.rb && sg.rb <= p.row_hi);
         segq[qtail % QN] = sg;
